@@ -1,0 +1,319 @@
+"""Benchmark of the balanced k-means hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl b200|reference]
+
+One step = one complete partition (SFC bootstrap + every movement iteration
+and balance round of Alg. 2) of the named synthetic configuration.
+
+  value : point-assignments/s (G/s) with inputs resident in HBM, timed with
+          CUDA events around each step (L2 flushed between steps);
+          point-assignments = the reference's total_decisions (one active
+          point processed in one balance round, kmeans.py:309).
+  e2e   : the same metric through the public API balanced_kmeans_points with
+          host numpy inputs (H2D of coords/weights and D2H of the int64
+          assignment inside the timed region).
+  roofline : the assign kernel (gp_assign_round), algorithmic bytes per
+          SURVEY §8d (B = n_act*(20+w_B) + n_scan*(8d+20)) over its
+          CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline : the CPU oracle (numpy restatement of the reference path) on a
+          bounded sample of the same workload, on this host.
+
+--impl reference times that CPU implementation alone (the reference is pure
+numpy; /root/reference does not exist on the GPU box, so the oracle port
+stands in for it).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+DESCR = {
+    "C1": "2D uniform n=100000, unit weights, k=16, eps=0.03",
+    "C2": "2D 32-component Gaussian mixture n=2^20, integer weights 1-60, k=64, eps=0.03",
+    "C3": "3D jittered 128^3 grid n=2^21, unit weights, k=256, eps=0.03",
+    "C4": "3D radially refined cloud n=2^24, float32 weights in [1,4], k=1024, eps=0.05",
+    "C5": "2D half uniform / half 1024-component mixture n=2^30, unit weights, k=16384, eps=0.03",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("GP_BENCH_CONFIG", "C2"))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload(cfg):
+    from paper_1805_01208_b200.workloads import CONFIGS, GENERATORS
+
+    c = CONFIGS[cfg]
+    pts, w = GENERATORS[cfg](seed=0)
+    return c, pts, w
+
+
+# ------------------------------------------------------------ CPU (oracle) arm
+def cpu_sample(cfg, c, pts, w, budget_s=25.0):
+    """Oracle on the same input: sample phase + as many full iterations as fit ~budget."""
+    from oracle import geographer_oracle as O
+
+    iters = 1
+    t0 = time.perf_counter()
+    r = O.run(pts, w, O.Knobs(k=c["k"], epsilon=c["epsilon"], seed=0, max_iter=iters),
+              scan_chunks=256)
+    dt = time.perf_counter() - t0
+    dec = sum(rec["total_decisions"] for rec in r.records)
+    if dt < budget_s / 3:
+        iters = max(1, min(50, int(budget_s / max(dt, 1e-3))))
+        t0 = time.perf_counter()
+        r = O.run(pts, w, O.Knobs(k=c["k"], epsilon=c["epsilon"], seed=0, max_iter=iters),
+                  scan_chunks=256)
+        dt = time.perf_counter() - t0
+        dec = sum(rec["total_decisions"] for rec in r.records)
+    return dict(value=dec / dt / 1e9, unit="Gpt/s", cores=1, kind="port",
+                sample=f"{cfg} input, full sample phase + {iters} full iteration(s) "
+                       f"(max_iter={iters}), oracle numpy single-threaded, 256 scan chunks; "
+                       f"{dec} point-assignments in {dt:.2f} s",
+                seconds=dt)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    c, pts, w = workload(args.config)
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(args.config, c, pts, w, budget_s=10.0)
+        if i >= args.warmup:
+            vals.append(s["value"])
+            last = s
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "point-assignments/s", "value": v, "unit": "Gpt/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": last["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SURVEY §8d recipe)",
+        "config": {"workload": f"{args.config}: {DESCR[args.config]}", "n": int(pts.shape[0]),
+                   "d": int(pts.shape[1]), "k": c["k"], "epsilon": c["epsilon"]},
+        "cpu_baseline": {"value": v, "unit": "Gpt/s", "cores": 1, "kind": "port",
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": "Gpt/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_b200(args):
+    import torch
+
+    from paper_1805_01208_b200 import KMeansSettings, balanced_kmeans_points
+    from paper_1805_01208_b200 import _native as N
+    from paper_1805_01208_b200.kmeans import _Timer, partition_device
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    c, pts, w = workload(args.config)
+    n, d = pts.shape
+    settings = KMeansSettings(k=c["k"], epsilon=c["epsilon"], seed=0)
+    pts_d = torch.from_numpy(pts).to(dev)
+    w_d = None if w is None else torch.from_numpy(w).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    N.reset_launch_count()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def step(timer=None):
+        a, stats = partition_device(pts_d, w_d, settings, device=dev, timer=timer)
+        return stats
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    times, decisions, timers = [], 0, []
+    N.reset_launch_count()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        barrier()
+        timer = _Timer()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        stats = step(timer)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+        timers.append((timer, stats))
+        decisions += sum(r.total_decisions for r in stats.iterations)
+    launches = N.launch_count()
+    clk = clocks.stop()
+    t_total = sum(times)
+    if dist is not None:
+        tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total = float(tt.item())
+        dd = torch.tensor([decisions], dtype=torch.float64, device=dev)
+        dist.all_reduce(dd)
+        decisions = float(dd.item())
+    value = decisions / t_total / 1e9
+
+    # roofline of the assign kernel
+    wb = 0 if w is None else 8
+    alg_bytes, kern_ms, flops = 0.0, 0.0, 0.0
+    for timer, stats in timers:
+        kern_ms += timer.total_ms()
+        for (nact, nscan, nev) in timer.rounds:
+            alg_bytes += nact * (4 + 16 + wb) + nscan * (8 * d + 20)
+            flops += nev * (3 * d + 1)
+    launches_assign = sum(len(t.events) for t, _ in timers)
+    peak, peak_kind = load_peaks()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e_t = []
+        for i in range(max(1, min(args.steps, 3)) + 1):
+            flush.fill_(1)
+            barrier()
+            t0 = time.perf_counter()
+            part, st2 = balanced_kmeans_points(pts, w, settings, return_stats=True)
+            torch.cuda.synchronize()
+            if i > 0:
+                e2e_t.append(time.perf_counter() - t0)
+        dec1 = sum(r.total_decisions for r in st2.iterations)
+        e2e = {"value": dec1 * world / max(e2e_t) / 1e9 if dist else dec1 / statistics.mean(e2e_t)
+               / 1e9, "unit": "Gpt/s",
+               "h2d_bytes_per_step": int(pts.nbytes + (0 if w is None else w.nbytes)),
+               "d2h_bytes_per_step": int(n * 8), "partition_s": statistics.mean(e2e_t)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(args.config, c, pts, w)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {
+            "metric": "point-assignments/s", "value": value, "unit": "Gpt/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SURVEY §8d recipe; paper meshes not available)",
+            "config": {"workload": f"{args.config}: {DESCR[args.config]}", "n": int(n),
+                       "d": int(d), "k": c["k"], "epsilon": c["epsilon"],
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "partition_s": t_total / args.steps},
+            "roofline": {"bound": "hbm", "kernel": "gp_assign_round",
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                         "traffic": None, "launches": launches_assign,
+                         "avg_launch_us": kern_ms * 1e3 / max(launches_assign, 1),
+                         "alg_bytes_per_launch": alg_bytes / max(launches_assign, 1),
+                         "fp64_flops_per_launch": flops / max(launches_assign, 1),
+                         "kernel_share_of_step": kern_ms / 1e3 / t_total},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches // max(args.steps, 1) if launches else None,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

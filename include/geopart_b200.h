@@ -1,0 +1,187 @@
+/*
+ * geopart_b200 — C ABI of the B200-native Geographer balanced k-means hot path.
+ *
+ * The reference (geopart, pure Python/numpy) has no FFI: its hot path is a set
+ * of per-rank numpy passes plus simulated collectives.  Each entry point below
+ * replaces one of those passes; the reference function it stands in for is
+ * cited next to it (paths relative to /root/reference/pkg/src/geopart).
+ *
+ * Conventions
+ *  - All pointers named in a signature are DEVICE pointers unless documented
+ *    otherwise; sizes are int64_t; `stream` is a cudaStream_t passed as void*.
+ *  - Every call is asynchronous on `stream` and returns GP_OK (0) or an error
+ *    code; gp_last_error() returns the thread-local message of the last error.
+ *  - The library never allocates or frees caller buffers.  Scratch is sized by
+ *    the *_workspace_bytes queries and passed in.
+ *  - Not re-entrant on the same buffers.
+ *  - Coordinates are float64.  Inputs in the caller's layout are described by
+ *    (stride_pt, stride_dim) in elements: AoS (n,d) row-major is (d, 1), SoA
+ *    (d,n) is (1, ld).  The library's own working layout is SoA (d rows of ld).
+ */
+#ifndef GEOPART_B200_H
+#define GEOPART_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GP_OK 0
+#define GP_ERR_INVALID 1
+#define GP_ERR_CUDA 2
+#define GP_ERR_NCCL 3
+
+#define GP_SEGMENTS 256 /* ranksim.py:38 */
+
+/* weight storage modes */
+#define GP_W_UNIT 0 /* weights None -> ones (ranksim.py:101-102) */
+#define GP_W_F32 1  /* every weight exactly representable as float32 */
+#define GP_W_F64 2
+
+const char* gp_last_error(void);
+int gp_abi_version(void);
+/* sizeof(gp_assign_args), sizeof(gp_fold_args): lets bindings verify struct layouts. */
+void gp_args_sizes(size_t* assign_args, size_t* fold_args);
+
+/* K1  global bounding box: replaces the per-shard min/max + allreduce_extreme
+ * of kmeans.py:546-548.  lohi[0:d] = min, lohi[d:2d] = max (device, doubles).
+ * *nonfinite (device int32) is set to 1 if any coordinate is NaN/inf. */
+int gp_box_minmax(const double* pts, int64_t n, int d, int64_t stride_pt, int64_t stride_dim,
+                  double* lohi, int32_t* nonfinite, void* stream);
+
+/* Weight probe (device): out[0] = flags (bit0 non-finite, bit1 not float32-exact),
+ * out[1] = min over nonzero |w| of the exponent of the lowest set mantissa bit,
+ * out[2] = bits of max |w| (double).  Used to choose exact integer block-weight
+ * accumulation. */
+int gp_weight_probe(const double* w, int64_t n, int64_t* out, void* stream);
+
+/* K2  Hilbert keys: replaces geometry.py:112-132 (point_cells) +
+ * geometry.py:135-179 (hilbert_cell_keys) + geometry.py:182-192.  Bit-exact.
+ * gids (nullable) receives gid_base + i. */
+int gp_hilbert_keys(const double* pts, int64_t n, int d, int64_t stride_pt, int64_t stride_dim,
+                    const double* lohi, int depth, uint64_t* keys, uint32_t* gids,
+                    uint32_t gid_base, void* stream);
+
+/* Host-side scalar helper (host pointers): Hilbert key of integer cells, same
+ * algorithm as the kernel; used by the host-logic tests. */
+uint64_t gp_hilbert_cell_key_host(const uint32_t* cells, int d, int depth);
+
+/* K3  stable LSD radix sort of (key, gid) pairs on the low key_bits bits:
+ * replaces np.lexsort((gids, keys)) in ranksim.py:158 (gids arrive in
+ * increasing order, so a stable key sort is the same total order). */
+int gp_sort_workspace_bytes(int64_t n, size_t* bytes);
+int gp_sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
+                  uint32_t* vals_out, int64_t n, int key_bits, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
+/* Payload gather after the sort: replaces the fancy-indexing redistribution of
+ * ranksim.py:159-168.  X (SoA, rows of ldx) <- pts[gids]; w_out (float or
+ * double per wmode; ignored for GP_W_UNIT) <- w_in[gids]. */
+int gp_gather_points(const double* pts, int64_t stride_pt, int64_t stride_dim, int d,
+                     const uint32_t* gids, int64_t n, double* X, int64_t ldx,
+                     const double* w_in, int wmode, void* w_out, void* stream);
+
+/* K4  initial centers: rows[i] = X[:, positions[i]] (kmeans.py:552-558). */
+int gp_gather_rows(const double* X, int64_t ldx, int d, const int64_t* positions, int k,
+                   double* rows, void* stream);
+
+/* K5  sample-phase active list: idx <- positions i (increasing) with
+ * rank[i] < size; *count (device int64).  Replaces kmeans.py:579 + the
+ * flatnonzero of kmeans.py:405-408. */
+int gp_compact_workspace_bytes(int64_t n, size_t* bytes);
+int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx,
+                      int64_t* count, void* workspace, size_t workspace_bytes, void* stream);
+
+/* K6  one assign round over the active points of one shard.  Replaces
+ * _scan_rank (kmeans.py:297-344) for every rank, the bound relaxations of
+ * kmeans.py:438-443 / :622-625 (applied lazily through per-cluster affine
+ * maps), and the block-weight segment sums of _global_block_weights
+ * (kmeans.py:368-374, ranksim.py:173-197) as exact int64 accumulation.
+ * The result per point is the lowest-index argmin of the reference's
+ * effective distance, bit for bit. */
+typedef struct gp_assign_args {
+  const double* X;        /* SoA coordinates, d rows of ldx */
+  int64_t ldx;
+  int32_t d;
+  int32_t k;
+  int32_t order3;         /* einsum summation order for d == 3 (see common.cuh) */
+  int32_t wmode;          /* GP_W_* */
+  const void* w;          /* weights (float or double) or NULL for unit */
+  double wscale;          /* exact scale 2^s: block weight units = w * wscale */
+  const int32_t* list;    /* active positions (NULL: all positions 0..m-1) */
+  int64_t m;              /* number of active entries */
+  int32_t* a;             /* assignment per position (-1 = unassigned) */
+  double* ub;             /* normalised upper bound per position */
+  double* lb;             /* normalised lower bound per position */
+  const double* centers;  /* k x d row-major */
+  const double* infl;     /* k influences */
+  const double* ub_scale; /* k: ub = ub_scale[a] * ub~ + ub_shift[a] */
+  const double* ub_shift; /* k */
+  double lb_scale;        /* lb = max(lb_scale * lb~ - lb_shift, 0) */
+  double lb_shift;
+  long long* block_w;     /* out: k exact block weights (units of 1/wscale), accumulated */
+  unsigned long long* counters; /* out: [skips, decisions, evals], accumulated */
+  double bound_err;       /* relative error bound of the host-composed maps: evaluated
+                             bounds are widened by bound_err * (|scale*b~| + |shift|) */
+} gp_assign_args;
+int gp_assign_round(const gp_assign_args* args, void* stream);
+
+/* Re-express every bound under identity maps (when the host's cumulative
+ * maps drift out of range).  Same bound semantics as gp_assign_args. */
+int gp_rebase_bounds(const gp_assign_args* args, void* stream);
+
+/* K7  movement reduction of one shard, bit-exact with the reference:
+ * per-(segment, block) sequential folds of w*x and w in SFC order
+ * (ranksim.py:173-197, kmeans.py:463-471), the sequential fold over segments
+ * (ranksim.py:218-222), per-block max distance to the old centers
+ * (_cluster_extents, kmeans.py:474-487) and the objective terms
+ * (kmeans.py:490-499).  Positions pos0..pos0+n_local-1 of a global sequence of
+ * n_global points; points with a < 0 are excluded. */
+typedef struct gp_fold_args {
+  const double* X;
+  int64_t ldx;
+  int32_t d;
+  int32_t k;
+  int32_t order3;
+  int32_t wmode;
+  const void* w;
+  const int32_t* a;
+  int64_t n_local;
+  int64_t pos0;           /* global position of local position 0 */
+  int64_t n_global;
+  const double* centers;  /* OLD centers (k x d) for extents and objective */
+  int32_t weights_only;   /* 1: fold only w (block weights in general-weight mode) */
+  /* outputs (device) */
+  double* sums;           /* k x d  : sum of w*x per block (only if !weights_only) */
+  double* wsum;           /* k      : sum of w per block */
+  double* extent;         /* k      : max distance to old center (only if !weights_only) */
+  double* objective;      /* k      : per-block objective partial (only if !weights_only) */
+  /* scratch */
+  void* workspace;
+  size_t workspace_bytes;
+} gp_fold_args;
+int gp_fold_workspace_bytes(int64_t n_local, int64_t pos0, int64_t n_global, int k,
+                            size_t* bytes);
+int gp_movement_fold(const gp_fold_args* args, void* stream);
+
+/* K8  bound audit (kmeans.py:347-365): brute-force n x k recheck of the
+ * bound contracts for the active points; out[3] += {audited, violations,
+ * bad_skips}.  Uses the same args as gp_assign_round (nothing written but out). */
+int gp_audit(const gp_assign_args* args, unsigned long long* out, void* stream);
+
+/* K9  result delivery: out[gids[i]] = a[i] (kmeans.py:637-641). */
+int gp_scatter_by_gid(const int32_t* a, const uint32_t* gids, int64_t n, int64_t* out,
+                      void* stream);
+
+/* Sample-rank delivery in SFC order: out[i] = rank_by_gid[gids[i]]
+ * (kmeans.py:568). */
+int gp_gather_ranks(const int32_t* rank_by_gid, const uint32_t* gids, int64_t n, int32_t* out,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEOPART_B200_H */

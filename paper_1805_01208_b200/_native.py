@@ -1,0 +1,129 @@
+"""ctypes binding of the C ABI in include/geopart_b200.h.
+
+There is no CPU fallback: importing this module loads libgeopart_b200.so and
+raises if it is missing, so a GPU box without the built extension fails
+loudly instead of silently running something else.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgeopart_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_1805_01208_b200.build` "
+        "(there is no CPU fallback)"
+    )
+lib = C.CDLL(LIB_PATH)
+
+i32, i64, u32, u64, f64, vp, sz = (C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double,
+                                   C.c_void_p, C.c_size_t)
+
+
+class AssignArgs(C.Structure):
+    _fields_ = [
+        ("X", vp), ("ldx", i64), ("d", i32), ("k", i32), ("order3", i32), ("wmode", i32),
+        ("w", vp), ("wscale", f64), ("list", vp), ("m", i64), ("a", vp), ("ub", vp), ("lb", vp),
+        ("centers", vp), ("infl", vp), ("ub_scale", vp), ("ub_shift", vp), ("lb_scale", f64),
+        ("lb_shift", f64), ("block_w", vp), ("counters", vp), ("bound_err", f64),
+    ]
+
+
+class FoldArgs(C.Structure):
+    _fields_ = [
+        ("X", vp), ("ldx", i64), ("d", i32), ("k", i32), ("order3", i32), ("wmode", i32),
+        ("w", vp), ("a", vp), ("n_local", i64), ("pos0", i64), ("n_global", i64),
+        ("centers", vp), ("weights_only", i32), ("sums", vp), ("wsum", vp), ("extent", vp),
+        ("objective", vp), ("workspace", vp), ("workspace_bytes", sz),
+    ]
+
+
+_SIGS = {
+    "gp_last_error": (C.c_char_p, []),
+    "gp_abi_version": (C.c_int, []),
+    "gp_args_sizes": (None, [C.POINTER(sz), C.POINTER(sz)]),
+    "gp_box_minmax": (C.c_int, [vp, i64, C.c_int, i64, i64, vp, vp, vp]),
+    "gp_weight_probe": (C.c_int, [vp, i64, vp, vp]),
+    "gp_hilbert_keys": (C.c_int, [vp, i64, C.c_int, i64, i64, vp, C.c_int, vp, vp, u32, vp]),
+    "gp_hilbert_cell_key_host": (u64, [C.POINTER(u32), C.c_int, C.c_int]),
+    "gp_sort_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_sort_pairs": (C.c_int, [vp, vp, vp, vp, i64, C.c_int, vp, sz, vp]),
+    "gp_gather_points": (C.c_int, [vp, i64, i64, C.c_int, vp, i64, vp, i64, vp, C.c_int, vp,
+                                   vp]),
+    "gp_gather_rows": (C.c_int, [vp, i64, C.c_int, vp, C.c_int, vp, vp]),
+    "gp_compact_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_compact_active": (C.c_int, [vp, i64, i64, vp, vp, vp, sz, vp]),
+    "gp_assign_round": (C.c_int, [C.POINTER(AssignArgs), vp]),
+    "gp_rebase_bounds": (C.c_int, [C.POINTER(AssignArgs), vp]),
+    "gp_audit": (C.c_int, [C.POINTER(AssignArgs), vp, vp]),
+    "gp_fold_workspace_bytes": (C.c_int, [i64, i64, i64, C.c_int, C.POINTER(sz)]),
+    "gp_movement_fold": (C.c_int, [C.POINTER(FoldArgs), vp]),
+    "gp_scatter_by_gid": (C.c_int, [vp, vp, i64, vp, vp]),
+    "gp_gather_ranks": (C.c_int, [vp, vp, i64, vp, vp]),
+}
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+def _verify_layouts():
+    a, f = sz(0), sz(0)
+    lib.gp_args_sizes(C.byref(a), C.byref(f))
+    if a.value != C.sizeof(AssignArgs) or f.value != C.sizeof(FoldArgs):
+        raise ImportError(f"struct layout mismatch: C {a.value}/{f.value} vs ctypes "
+                          f"{C.sizeof(AssignArgs)}/{C.sizeof(FoldArgs)}")
+
+
+_verify_layouts()
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = lib.gp_last_error().decode(errors="replace")
+        raise NativeError(f"{what or 'geopart_b200'}: error {rc}: {msg}")
+
+
+# kernels launched per API call (bench.py's gpu_launches claim); CUB's sort is
+# counted as one histogram pass plus one launch per 8-bit digit pass
+KERNELS_PER_CALL = {
+    "gp_box_minmax": 2, "gp_weight_probe": 1, "gp_hilbert_keys": 1, "gp_sort_pairs": 9,
+    "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 3,
+    "gp_assign_round": 1, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 5,
+    "gp_scatter_by_gid": 1, "gp_gather_ranks": 1,
+}
+_launches = [0]
+
+
+def reset_launch_count() -> None:
+    _launches[0] = 0
+
+
+def launch_count() -> int:
+    return _launches[0]
+
+
+def count(name: str) -> None:
+    _launches[0] += KERNELS_PER_CALL.get(name, 0)
+
+
+def call(name: str, *args) -> None:
+    count(name)
+    check(getattr(lib, name)(*args), name)
+
+
+def size_query(name: str, *args) -> int:
+    out = sz(0)
+    check(getattr(lib, name)(*args, C.byref(out)), name)
+    return int(out.value)

@@ -1,0 +1,168 @@
+"""Host-side k-sized control math of the balance / movement loops.
+
+All of it is O(k) numpy run between kernel launches.  It must produce the
+reference's bits: the reference computes these quantities with numpy on the
+host (kmeans.py:170-239, metrics.py:26-40), so this module applies the very
+same numpy operations in the same order.  Nothing here touches per-point data.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import replace
+
+import numpy as np
+
+from .types import ClusterState, GraphError, PointBounds
+
+UB_SLACK = 1.0 + 1e-12  # kmeans.py:61
+LB_SLACK = 1.0 - 1e-12  # kmeans.py:62
+
+
+def balance_target(total_weight: float, k: int) -> float:
+    """metrics.py:26-30: ceil(total / k), integer ceil when the total is integral."""
+    if float(total_weight).is_integer():
+        return float(-(-int(total_weight) // k))
+    return float(math.ceil(total_weight / k))
+
+
+def imbalance(block_weights) -> float:
+    """metrics.py:33-40: max / ceil(total/k) - 1."""
+    bw = np.asarray(block_weights, dtype=np.float64)
+    total = float(bw.sum())
+    if total <= 0:
+        raise GraphError("total weight must be positive")
+    return float(bw.max() / balance_target(total, bw.shape[0]) - 1.0)
+
+
+def initial_center_positions(n: int, k: int) -> np.ndarray:
+    """kmeans.py:170-173: floor(i*n/k + n/(2k)) as ((2i+1) n) // (2k)."""
+    i = np.arange(k, dtype=np.int64)
+    return ((2 * i + 1) * n) // (2 * k)
+
+
+def influence_factor(block_w: np.ndarray, target: float, cap: float, dim: int) -> np.ndarray:
+    """Multiplicative influence step of kmeans.py:187-190."""
+    with np.errstate(divide="ignore"):
+        gamma = np.where(block_w > 0, target / np.where(block_w > 0, block_w, 1.0), np.inf)
+    return np.clip(gamma ** (1.0 / dim), 1.0 - cap, 1.0 + cap)
+
+
+def adapt_influence(state: ClusterState, target_weight: float, cap: float) -> ClusterState:
+    if not 0 < cap < 1:
+        raise ValueError("cap must lie in (0, 1)")
+    if not target_weight > 0:
+        raise ValueError("target weight must be positive")
+    step = influence_factor(state.block_weights, target_weight, cap, state.dim)
+    return replace(state, influence=state.influence * step)
+
+
+def eroded(influence: np.ndarray, moves: np.ndarray, beta: float) -> np.ndarray:
+    """kmeans.py:204-205: influence ** (1 - alpha), alpha = 2/(1+exp(-delta/beta)) - 1."""
+    alpha = 2.0 / (1.0 + np.exp(-moves / beta)) - 1.0
+    return influence ** (1.0 - alpha)
+
+
+def erode_influence(state: ClusterState, beta: float) -> ClusterState:
+    if not beta > 0:
+        raise ValueError("beta must be strictly positive")
+    return replace(state, influence=eroded(state.influence, state.last_move, beta))
+
+
+def effective_distance(p, center, influence: float) -> float:
+    """kmeans.py:150-154."""
+    if not influence > 0:
+        raise ValueError("influence must be strictly positive")
+    d = np.asarray(p, dtype=np.float64) - np.asarray(center, dtype=np.float64)
+    return math.sqrt(float(np.dot(d, d))) / influence
+
+
+def relax_is_identity(old_infl, new_infl, moves) -> bool:
+    """The early return of kmeans.py:223-228."""
+    return moves.shape == old_infl.shape and not moves.any() and np.array_equal(old_infl, new_infl)
+
+
+def relax_bounds(bounds: PointBounds, assignment, old_influence, new_influence,
+                 center_moves) -> PointBounds:
+    """Eager array form of the bound relaxation (kmeans.py:208-239), for API parity.
+
+    The device path never materialises this per point; it composes the same
+    affine maps lazily (:class:`BoundMaps`).
+    """
+    if relax_is_identity(old_influence, new_influence, center_moves):
+        return bounds
+    ratio = old_influence / new_influence
+    shift = center_moves / new_influence
+    assignment = np.asarray(assignment)
+    has = assignment >= 0
+    c = np.where(has, assignment, 0)
+    upper = np.where(has, (bounds.upper * ratio[c] + shift[c]) * UB_SLACK, bounds.upper)
+    lower = np.maximum((bounds.lower * ratio.min() - shift.max()) * LB_SLACK, 0.0)
+    return PointBounds(upper=upper, lower=lower)
+
+
+def sample_schedule(n: int, init_sample: int) -> list[int]:
+    """kmeans.py:456-460."""
+    if init_sample <= 0 or n <= init_sample:
+        return []
+    rounds = math.ceil(math.log2(n / init_sample))
+    return [init_sample * 2**j for j in range(rounds)]
+
+
+class BoundMaps:
+    """Cumulative affine maps standing in for per-point eager relaxation.
+
+    A point scanned when the maps were (S_c, T_c) / (A, B) stores
+    ub~ = (best - T_c)/S_c and lb~ = (second + B)/A.  Each relaxation of
+    kmeans.py:229-238 is affine in the bound (ub' = (ub*r_c + s_c)*UB_SLACK and
+    lb' = max((lb*min r - max s)*LB_SLACK, 0)), so composing the maps instead
+    of rewriting n bounds gives the same sound bounds.  Host rounding in the
+    composition is at most ~3 ulps per step relative to each of scale and
+    shift; the device widens every evaluated bound by
+    ``bound_err * (|scale * b~| + |shift|)`` with ``bound_err`` covering all
+    steps since the last reset, which matters only where the affine form
+    cancels (bounds near zero; e.g. a point sitting on its center).
+    """
+
+    def __init__(self, k: int):
+        self.ub_scale = np.ones(k)
+        self.ub_shift = np.zeros(k)
+        self.lb_scale = 1.0
+        self.lb_shift = 0.0
+        self.version = 0
+        self.steps = 0
+
+    def relax(self, old_infl, new_infl, moves) -> bool:
+        if relax_is_identity(old_infl, new_infl, moves):
+            return False
+        ratio = old_infl / new_infl
+        shift = moves / new_infl
+        self.ub_scale = self.ub_scale * ratio * UB_SLACK
+        self.ub_shift = (self.ub_shift * ratio + shift) * UB_SLACK
+        rmin = float(ratio.min())
+        smax = float(shift.max())
+        self.lb_scale = float(self.lb_scale * rmin * LB_SLACK)
+        self.lb_shift = float((self.lb_shift * rmin + smax) * LB_SLACK)
+        self.version += 1
+        self.steps += 1
+        return True
+
+    @property
+    def bound_err(self) -> float:
+        return (4.0 * self.steps + 16.0) * 2.0 ** -52
+
+    def needs_rebase(self, scale_hint: float) -> bool:
+        lim = 1e6
+        s = self.ub_scale
+        return bool(
+            s.min() < 1 / lim or s.max() > lim or not (1 / lim < self.lb_scale < lim)
+            or self.ub_shift.max() > 64.0 * scale_hint or self.lb_shift > 64.0 * scale_hint
+        )
+
+    def reset(self):
+        self.ub_scale[:] = 1.0
+        self.ub_shift[:] = 0.0
+        self.lb_scale = 1.0
+        self.lb_shift = 0.0
+        self.version += 1
+        self.steps = 0

@@ -1,0 +1,111 @@
+// Shared helpers for the geopart-b200 sm_100a kernels.
+//
+// Every fp64 operation whose bits must equal the reference's numpy result is
+// written with an explicit round-to-nearest intrinsic (__dsub_rn, __dmul_rn,
+// __dadd_rn, __dsqrt_rn, __ddiv_rn): those are never contracted into FMA,
+// whatever -fmad says, so the kernels reproduce numpy's separately rounded
+// ufunc arithmetic.  Pruning bounds use directed rounding (_ru / _rd) so that
+// they stay rigorous.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/geopart_b200.h"
+
+namespace gp {
+
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+#define GP_REQUIRE(cond, ...)            \
+  do {                                   \
+    if (!(cond)) {                       \
+      ::gp::set_error(__VA_ARGS__);      \
+      return GP_ERR_INVALID;             \
+    }                                    \
+  } while (0)
+
+#define GP_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t _e = (call);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      ::gp::set_error("%s failed: %s", #call, cudaGetErrorString(_e));             \
+      return GP_ERR_CUDA;                                                          \
+    }                                                                              \
+  } while (0)
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Squared Euclidean norm of a difference vector in the summation order the
+// host numpy einsum('ij,ij->i') uses (probed at import).
+//   2D: dx^2 + dy^2
+//   3D: order 0: (x+y)+z   1: (x+z)+y   2: (y+z)+x
+__device__ __forceinline__ double sqnorm_rn(const double* v, int d, int order3) {
+  double xx = __dmul_rn(v[0], v[0]);
+  double yy = __dmul_rn(v[1], v[1]);
+  if (d == 2) return __dadd_rn(xx, yy);
+  double zz = __dmul_rn(v[2], v[2]);
+  if (order3 == 1) return __dadd_rn(__dadd_rn(xx, zz), yy);
+  if (order3 == 2) return __dadd_rn(__dadd_rn(yy, zz), xx);
+  return __dadd_rn(__dadd_rn(xx, yy), zz);
+}
+
+// Reference effective distance sqrt(einsum(diff, diff)) / influence
+// (kmeans.py:157-159), bit for bit.
+template <int D>
+__device__ __forceinline__ double effdist_rn(const double* p, const double* c, double infl,
+                                             int order3) {
+  double diff[3];
+#pragma unroll
+  for (int j = 0; j < D; ++j) diff[j] = __dsub_rn(p[j], c[j]);
+  return __ddiv_rn(__dsqrt_rn(sqnorm_rn(diff, D, order3)), infl);
+}
+
+// Order-preserving map from doubles to unsigned 64-bit keys (for atomic min/max).
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+  unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+__host__ __device__ __forceinline__ unsigned long long dkey_host_min() { return ~0ull; }
+
+// Lazily relaxed Hamerly bounds: ub = S[a]*ub~ + T[a] and
+// lb = max(A*lb~ - B, 0), evaluated with one directed rounding (FMA) and widened
+// by the host composition error err*(|S*ub~| + |T|) so cancellation near zero
+// can never make them unsound.
+__device__ __forceinline__ double ub_eval(double S, double u, double T, double err) {
+  double v = __fma_ru(S, u, T);
+  double mag = __dadd_ru(fabs(__dmul_ru(S, u)), fabs(T));
+  return __fma_ru(err, mag, v);
+}
+__device__ __forceinline__ double lb_eval(double A, double l, double B, double err) {
+  if (isinf(l)) return l;  // k == 1: no runner-up
+  double v = __fma_rd(A, l, -B);
+  double mag = __dadd_ru(__dmul_ru(A, l), B);
+  return fmax(__fma_rd(-err, mag, v), 0.0);
+}
+
+__device__ __forceinline__ double load_weight(const void* w, int wmode, int64_t i) {
+  if (wmode == GP_W_UNIT) return 1.0;
+  if (wmode == GP_W_F32) return (double)((const float*)w)[i];
+  return ((const double*)w)[i];
+}
+
+// Segment (of GP_SEGMENTS equal position ranges, ranksim.py:74-75) of a global
+// position: the largest s with floor(s*n/S) <= pos.
+__device__ __forceinline__ int segment_of(int64_t pos, int64_t n) {
+  return (int)(((pos + 1) * (int64_t)GP_SEGMENTS - 1) / n);
+}
+
+inline unsigned grid_for(int64_t work, int per_block, int cap = 1 << 30) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+}  // namespace gp

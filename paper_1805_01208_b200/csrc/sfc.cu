@@ -1,0 +1,452 @@
+// SFC bootstrap kernels: bounding box, Hilbert keys, radix sort, payload
+// gather, initial centers, sample-phase compaction, result scatter.
+//
+// Reference semantics: geometry.py:112-192 (cells + Hilbert keys),
+// ranksim.py:143-170 (global sort + redistribution), kmeans.py:546-568.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace gp {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s launch failed: %s", what, cudaGetErrorString(e));
+    return GP_ERR_CUDA;
+  }
+  return GP_OK;
+}
+
+// ---------------------------------------------------------------- K1 box
+__global__ void box_kernel(const double* __restrict__ pts, int64_t n, int d, int64_t sp,
+                           int64_t sd, unsigned long long* keys, int32_t* nonfinite) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY};
+  double hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int j = 0; j < d; ++j) {
+      double v = pts[i * sp + j * sd];
+      bad |= !isfinite(v);
+      lo[j] = fmin(lo[j], v);
+      hi[j] = fmax(hi[j], v);
+    }
+  }
+  for (int j = 0; j < d; ++j) {
+    for (int o = 16; o; o >>= 1) {
+      lo[j] = fmin(lo[j], __shfl_xor_sync(FULL, lo[j], o));
+      hi[j] = fmax(hi[j], __shfl_xor_sync(FULL, hi[j], o));
+    }
+  }
+  bad = __any_sync(FULL, bad);
+  if ((threadIdx.x & 31) == 0) {
+    for (int j = 0; j < d; ++j) {
+      atomicMin(&keys[j], dkey(lo[j]));
+      atomicMax(&keys[d + j], dkey(hi[j]));
+    }
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
+__global__ void box_finalize(unsigned long long* keys, int d) {
+  int j = threadIdx.x;
+  if (j < 2 * d) {
+    double v = dkey_inv(keys[j]);
+    reinterpret_cast<double*>(keys)[j] = v;
+  }
+}
+
+// ------------------------------------------------------- weight probe
+__global__ void weight_probe_kernel(const double* __restrict__ w, int64_t n,
+                                    unsigned long long* out) {
+  unsigned long long flags = 0;
+  int low = 4096;
+  double mx = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = w[i];
+    if (!isfinite(v)) { flags |= 1; continue; }
+    if ((double)(float)v != v) flags |= 2;
+    double av = fabs(v);
+    mx = fmax(mx, av);
+    if (av != 0.0) {
+      // exponent of the lowest set bit: av = m * 2^e with m odd
+      int e;
+      double m = frexp(av, &e);  // av = m * 2^e, m in [0.5, 1)
+      // ldexp(m, 53) is an integer in [2^52, 2^53) (exact): av = iv * 2^(e-53)
+      unsigned long long iv = (unsigned long long)ldexp(m, 53);
+      int tz = __ffsll((long long)iv) - 1;
+      low = min(low, e - 53 + tz);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    flags |= __shfl_xor_sync(FULL, flags, o);
+    low = min(low, __shfl_xor_sync(FULL, low, o));
+    mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&out[0], flags);
+    atomicMin((long long*)&out[1], (long long)low);
+    atomicMax(&out[2], (unsigned long long)__double_as_longlong(mx));
+  }
+}
+
+// -------------------------------------------------------- K2 Hilbert keys
+__device__ __forceinline__ uint64_t spread2(uint32_t x) {
+  uint64_t v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+__device__ __forceinline__ uint64_t spread3(uint32_t x) {
+  uint64_t v = x & 0x1fffffu;
+  v = (v | (v << 32)) & 0x001f00000000ffffull;
+  v = (v | (v << 16)) & 0x001f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+// geometry.py:135-179 on 32-bit lanes (cells < 2^depth <= 2^31).
+template <int D>
+__host__ __device__ __forceinline__ void hilbert_transpose(uint32_t* X, int depth) {
+  for (uint32_t Q = 1u << (depth - 1); Q > 1; Q >>= 1) {
+    uint32_t P = Q - 1;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      uint32_t t = (X[0] ^ X[i]) & P;
+      bool flip = (X[i] & Q) != 0;
+      X[0] ^= flip ? P : t;
+      if (!flip) X[i] ^= t;
+    }
+  }
+#pragma unroll
+  for (int i = 1; i < D; ++i) X[i] ^= X[i - 1];
+  uint32_t t = 0;
+  for (uint32_t Q = 1u << (depth - 1); Q > 1; Q >>= 1)
+    if (X[D - 1] & Q) t ^= Q - 1;
+#pragma unroll
+  for (int i = 0; i < D; ++i) X[i] ^= t;
+}
+
+template <int D>
+__device__ __forceinline__ uint64_t interleave(const uint32_t* X) {
+  if (D == 2) return (spread2(X[0]) << 1) | spread2(X[1]);
+  return (spread3(X[0]) << 2) | (spread3(X[1]) << 1) | spread3(X[2]);
+}
+
+template <int D>
+__global__ void hilbert_kernel(const double* __restrict__ pts, int64_t n, int64_t sp, int64_t sd,
+                               const double* __restrict__ lohi, int depth,
+                               uint64_t* __restrict__ keys, uint32_t* __restrict__ gids,
+                               uint32_t gid_base) {
+  double lo[D], safe[D];
+  const double side = (double)(1ull << depth);
+  const double top = side - 1.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    lo[j] = lohi[j];
+    double ext = __dsub_rn(lohi[D + j], lo[j]);
+    safe[j] = ext > 0.0 ? ext : 1.0;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t X[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      // geometry.py:129-132: (p - lo) / ext * 2^depth, floor, clip to [0, side-1]
+      double s = __dmul_rn(__ddiv_rn(__dsub_rn(pts[i * sp + j * sd], lo[j]), safe[j]), side);
+      double c = fmin(fmax(floor(s), 0.0), top);
+      X[j] = (uint32_t)c;
+    }
+    hilbert_transpose<D>(X, depth);
+    keys[i] = interleave<D>(X);
+    if (gids) gids[i] = gid_base + (uint32_t)i;
+  }
+}
+
+// ---------------------------------------------------------- payload gather
+__global__ void gather_points_kernel(const double* __restrict__ pts, int64_t sp, int64_t sd, int d,
+                                     const uint32_t* __restrict__ gids, int64_t n,
+                                     double* __restrict__ X, int64_t ldx,
+                                     const double* __restrict__ w_in, int wmode, void* w_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g = gids[i];
+    for (int j = 0; j < d; ++j) X[j * ldx + i] = pts[g * sp + j * sd];
+    if (wmode == GP_W_F32) ((float*)w_out)[i] = (float)w_in[g];
+    else if (wmode == GP_W_F64) ((double*)w_out)[i] = w_in[g];
+  }
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ X, int64_t ldx, int d,
+                                   const int64_t* __restrict__ pos, int k, double* rows) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k)
+    for (int j = 0; j < d; ++j) rows[i * d + j] = X[j * ldx + pos[i]];
+}
+
+// ------------------------------------------------------- K5 compaction
+constexpr int CT_THREADS = 256;
+constexpr int CT_ROUNDS = 16;
+constexpr int CT_TILE = CT_THREADS * CT_ROUNDS;
+
+__global__ void compact_count(const int32_t* __restrict__ rank, int64_t n, int64_t size,
+                              int64_t* counts) {
+  int64_t base = (int64_t)blockIdx.x * CT_TILE;
+  int c = 0;
+  for (int r = 0; r < CT_ROUNDS; ++r) {
+    int64_t i = base + r * CT_THREADS + threadIdx.x;
+    c += (i < n && rank[i] < size);
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  __shared__ int ws[CT_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < CT_THREADS / 32; ++w) t += ws[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+__global__ void exclusive_scan_serial(int64_t* counts, int64_t m, int64_t* total) {
+  // single block: chunked scan
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < m; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < m ? counts[i] : 0;
+    // block inclusive scan (Hillis-Steele in smem)
+    __shared__ int64_t buf[1024];
+    buf[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+      int64_t t = threadIdx.x >= (unsigned)o ? buf[threadIdx.x - o] : 0;
+      __syncthreads();
+      buf[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < m) counts[i] = carry + buf[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += buf[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void compact_write(const int32_t* __restrict__ rank, int64_t n, int64_t size,
+                              const int64_t* __restrict__ offsets, int32_t* __restrict__ idx) {
+  __shared__ int wsum[CT_THREADS / 32];
+  __shared__ int64_t run;
+  int64_t base = (int64_t)blockIdx.x * CT_TILE;
+  if (threadIdx.x == 0) run = offsets[blockIdx.x];
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  for (int r = 0; r < CT_ROUNDS; ++r) {
+    int64_t i = base + r * CT_THREADS + threadIdx.x;
+    bool f = i < n && rank[i] < size;
+    unsigned b = __ballot_sync(FULL, f);
+    if (lane == 0) wsum[warp] = __popc(b);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < CT_THREADS / 32; ++w) {
+      before += (w < warp) ? wsum[w] : 0;
+      tot += wsum[w];
+    }
+    if (f) idx[run + before + __popc(b & ((1u << lane) - 1))] = (int32_t)i;
+    __syncthreads();
+    if (threadIdx.x == 0) run += tot;
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------- scatter / gather
+__global__ void scatter_gid_kernel(const int32_t* __restrict__ a, const uint32_t* __restrict__ g,
+                                   int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[g[i]] = a[i];
+}
+
+__global__ void gather_ranks_kernel(const int32_t* __restrict__ r, const uint32_t* __restrict__ g,
+                                    int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = r[g[i]];
+}
+
+static unsigned stride_grid(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)sms * 8;
+  return (unsigned)(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+}  // namespace gp
+
+using namespace gp;
+
+extern "C" {
+
+const char* gp_last_error(void) { return g_err; }
+int gp_abi_version(void) { return 1; }
+void gp_args_sizes(size_t* a, size_t* f) {
+  *a = sizeof(gp_assign_args);
+  *f = sizeof(gp_fold_args);
+}
+
+int gp_box_minmax(const double* pts, int64_t n, int d, int64_t stride_pt, int64_t stride_dim,
+                  double* lohi, int32_t* nonfinite, void* stream) {
+  GP_REQUIRE(n >= 1, "gp_box_minmax: n must be >= 1");
+  GP_REQUIRE(d == 2 || d == 3, "gp_box_minmax: d must be 2 or 3");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(lohi);
+  GP_CUDA(cudaMemsetAsync(keys, 0xff, d * sizeof(double), s));
+  GP_CUDA(cudaMemsetAsync(keys + d, 0x00, d * sizeof(double), s));
+  GP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
+  box_kernel<<<stride_grid(n), 256, 0, s>>>(pts, n, d, stride_pt, stride_dim, keys, nonfinite);
+  box_finalize<<<1, 32, 0, s>>>(keys, d);
+  return check_launch("box");
+}
+
+int gp_weight_probe(const double* w, int64_t n, int64_t* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t init[3] = {0, 4096, 0};
+  GP_CUDA(cudaMemcpyAsync(out, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  if (n > 0)
+    weight_probe_kernel<<<stride_grid(n), 256, 0, s>>>(w, n, (unsigned long long*)out);
+  return check_launch("weight_probe");
+}
+
+int gp_hilbert_keys(const double* pts, int64_t n, int d, int64_t stride_pt, int64_t stride_dim,
+                    const double* lohi, int depth, uint64_t* keys, uint32_t* gids,
+                    uint32_t gid_base, void* stream) {
+  GP_REQUIRE(d == 2 || d == 3, "gp_hilbert_keys: unsupported dimension %d", d);
+  GP_REQUIRE(depth >= 1 && d * depth <= 62, "gp_hilbert_keys: depth %d out of range for d=%d",
+             depth, d);
+  if (n == 0) return GP_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d == 2)
+    hilbert_kernel<2><<<stride_grid(n), 256, 0, s>>>(pts, n, stride_pt, stride_dim, lohi, depth,
+                                                     keys, gids, gid_base);
+  else
+    hilbert_kernel<3><<<stride_grid(n), 256, 0, s>>>(pts, n, stride_pt, stride_dim, lohi, depth,
+                                                     keys, gids, gid_base);
+  return check_launch("hilbert_keys");
+}
+
+uint64_t gp_hilbert_cell_key_host(const uint32_t* cells, int d, int depth) {
+  uint32_t X[3] = {cells[0], cells[1], d == 3 ? cells[2] : 0u};
+  if (d == 2) hilbert_transpose<2>(X, depth);
+  else hilbert_transpose<3>(X, depth);
+  uint64_t key = 0;
+  for (int j = depth - 1; j >= 0; --j)
+    for (int i = 0; i < d; ++i) key = (key << 1) | ((X[i] >> j) & 1u);
+  return key;
+}
+
+int gp_sort_workspace_bytes(int64_t n, size_t* bytes) {
+  GP_REQUIRE(n >= 0 && n < (1ll << 31), "gp_sort: n out of range");
+  size_t b = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint64_t*)nullptr,
+                                                  (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                                  (uint32_t*)nullptr, (int)n, 0, 64);
+  if (e != cudaSuccess) {
+    set_error("sort workspace query failed: %s", cudaGetErrorString(e));
+    return GP_ERR_CUDA;
+  }
+  *bytes = b;
+  return GP_OK;
+}
+
+int gp_sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
+                  uint32_t* vals_out, int64_t n, int key_bits, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  GP_REQUIRE(key_bits >= 1 && key_bits <= 64, "gp_sort: key_bits out of range");
+  GP_REQUIRE(n >= 0 && n < (1ll << 31), "gp_sort: n out of range");
+  if (n == 0) return GP_OK;
+  size_t b = workspace_bytes;
+  GP_CUDA(cub::DeviceRadixSort::SortPairs(workspace, b, keys_in, keys_out, vals_in, vals_out,
+                                          (int)n, 0, key_bits, (cudaStream_t)stream));
+  return check_launch("sort_pairs");
+}
+
+int gp_gather_points(const double* pts, int64_t stride_pt, int64_t stride_dim, int d,
+                     const uint32_t* gids, int64_t n, double* X, int64_t ldx, const double* w_in,
+                     int wmode, void* w_out, void* stream) {
+  GP_REQUIRE(d == 2 || d == 3, "gp_gather_points: bad d");
+  GP_REQUIRE(wmode == GP_W_UNIT || (w_in && w_out), "gp_gather_points: weights missing");
+  if (n == 0) return GP_OK;
+  gather_points_kernel<<<stride_grid(n), 256, 0, (cudaStream_t)stream>>>(
+      pts, stride_pt, stride_dim, d, gids, n, X, ldx, w_in, wmode, w_out);
+  return check_launch("gather_points");
+}
+
+int gp_gather_rows(const double* X, int64_t ldx, int d, const int64_t* positions, int k,
+                   double* rows, void* stream) {
+  GP_REQUIRE(k >= 1, "gp_gather_rows: k must be >= 1");
+  gather_rows_kernel<<<grid_for(k, 256), 256, 0, (cudaStream_t)stream>>>(X, ldx, d, positions, k,
+                                                                          rows);
+  return check_launch("gather_rows");
+}
+
+int gp_compact_workspace_bytes(int64_t n, size_t* bytes) {
+  int64_t tiles = (n + CT_TILE - 1) / CT_TILE;
+  *bytes = (size_t)(tiles + 1) * sizeof(int64_t);
+  return GP_OK;
+}
+
+int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx, int64_t* count,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  int64_t tiles = (n + CT_TILE - 1) / CT_TILE;
+  GP_REQUIRE(workspace_bytes >= (size_t)(tiles + 1) * sizeof(int64_t),
+             "gp_compact_active: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    GP_CUDA(cudaMemsetAsync(count, 0, sizeof(int64_t), s));
+    return GP_OK;
+  }
+  int64_t* counts = (int64_t*)workspace;
+  compact_count<<<(unsigned)tiles, CT_THREADS, 0, s>>>(rank, n, size, counts);
+  exclusive_scan_serial<<<1, 1024, 0, s>>>(counts, tiles, count);
+  compact_write<<<(unsigned)tiles, CT_THREADS, 0, s>>>(rank, n, size, counts, idx);
+  return check_launch("compact_active");
+}
+
+int gp_scatter_by_gid(const int32_t* a, const uint32_t* gids, int64_t n, int64_t* out,
+                      void* stream) {
+  if (n == 0) return GP_OK;
+  scatter_gid_kernel<<<stride_grid(n), 256, 0, (cudaStream_t)stream>>>(a, gids, n, out);
+  return check_launch("scatter_by_gid");
+}
+
+int gp_gather_ranks(const int32_t* rank_by_gid, const uint32_t* gids, int64_t n, int32_t* out,
+                    void* stream) {
+  if (n == 0) return GP_OK;
+  gather_ranks_kernel<<<stride_grid(n), 256, 0, (cudaStream_t)stream>>>(rank_by_gid, gids, n,
+                                                                        out);
+  return check_launch("gather_ranks");
+}
+
+}  // extern "C"

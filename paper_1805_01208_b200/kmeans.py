@@ -1,0 +1,468 @@
+"""Drop-in balanced k-means partitioner on B200 (arXiv 1805.01208, Alg. 1 + Alg. 2).
+
+Public entry points keep the reference's signatures
+(``balanced_kmeans_points`` kmeans.py:502-512, ``balanced_kmeans``
+kmeans.py:515-534).  The host loop below mirrors ``_run_pipeline``
+(kmeans.py:537-650) and ``assign_and_balance`` (kmeans.py:377-453) line for
+line for every k-sized decision, in host numpy; every n-sized pass runs in the
+sm_100a kernels of ``csrc/`` through the C ABI:
+
+  reference pass                                 device call
+  ---------------------------------------------  ---------------------------
+  min/max + allreduce_extreme  kmeans.py:546-548 gp_box_minmax
+  hilbert_keys                 geometry.py:182   gp_hilbert_keys
+  global_sort_redistribute     ranksim.py:143    gp_sort_pairs + gp_gather_points
+  gather_rows (initial centers) kmeans.py:552    gp_gather_rows
+  active = rank < size         kmeans.py:579     gp_compact_active
+  _scan_rank + relax_bounds + _global_block_weights
+                               kmeans.py:297-453 gp_assign_round (per balance round)
+  _weighted_center_partials + weighted_mean_reduce + _cluster_extents + _objective
+                               kmeans.py:463-499 gp_movement_fold
+  _audit_rank                  kmeans.py:347     gp_audit
+  full_assignment[gids] = a    kmeans.py:637     gp_scatter_by_gid
+
+There is no CPU fallback: without the built extension the import fails.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .control import (
+    BoundMaps,
+    imbalance,
+    influence_factor,
+    eroded,
+    initial_center_positions,
+    sample_schedule,
+)
+from .numerics import einsum_order3
+from .types import (
+    BalanceInfo,
+    BoundingBox,
+    ClusterState,
+    GeometryError,
+    IterationRecord,
+    KMeansSettings,
+    KMeansStats,
+    Partition,
+)
+
+DEFAULT_DEPTH = {2: 31, 3: 20}  # geometry.py:28
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class RankWorld:
+    """Rank-count descriptor kept for API parity with ranksim.RankWorld.
+
+    Results are identical for every p (as in the reference for p | 256); on
+    one GPU p only validates.  Multi-GPU runs shard by SFC range across the
+    processes of a torch.distributed group (see parallel.py).
+    """
+
+    def __init__(self, n: int, dim: int, p: int, coords=None, weights=None):
+        self.n, self.dim, self.p = n, dim, p
+        self.coords, self.weights = coords, weights
+
+    @classmethod
+    def from_points(cls, points, weights=None, p: int = 1) -> "RankWorld":
+        n = int(points.shape[0])
+        if p < 1 or p > n:
+            raise ValueError(f"rank count {p} out of range 1..{n}")
+        dim = int(points.shape[1]) if len(points.shape) > 1 else 0
+        return cls(n, dim, p, points, weights)
+
+    @classmethod
+    def from_graph(cls, graph, p: int = 1) -> "RankWorld":
+        return cls.from_points(graph.coords, graph.vertex_weights, p)
+
+
+@dataclass
+class _WeightPlan:
+    mode: int          # GP_W_*
+    exact: bool        # block-weight sums exact in int64 units of 1/scale
+    scale: float       # 2^s
+
+
+class _Timer:
+    """Optional CUDA-event timing of the assign kernel (for bench.py's roofline)."""
+
+    def __init__(self):
+        self.events = []
+        self.rounds = []   # (n_active, n_scanned, n_evals) per assign launch
+
+    def mark(self, stream):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        return ev
+
+    def total_ms(self) -> float:
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in self.events)
+
+
+class DevicePartitioner:
+    """One partition run on one GPU (the whole point set is one SFC shard)."""
+
+    def __init__(self, settings: KMeansSettings, device=None, timer: _Timer | None = None):
+        self.settings = settings
+        self.device = torch.device(device if device is not None else "cuda")
+        self.timer = timer
+        self.order3 = einsum_order3()
+        self.stream = torch.cuda.current_stream(self.device)
+        self.sh = self.stream.cuda_stream
+
+    # ------------------------------------------------------------ bootstrap
+    def _input(self, points, weights):
+        dev = self.device
+        if isinstance(points, torch.Tensor):
+            pts = points.to(device=dev, dtype=torch.float64)
+        else:
+            pts = torch.from_numpy(np.ascontiguousarray(np.asarray(points, dtype=np.float64)))
+            pts = pts.to(dev)
+        if pts.dim() != 2:
+            raise GeometryError("points must be an (n, d) array")
+        w = None
+        if weights is not None:
+            if isinstance(weights, torch.Tensor):
+                w = weights.to(device=dev, dtype=torch.float64).contiguous()
+            else:
+                w = torch.from_numpy(np.ascontiguousarray(np.asarray(weights, dtype=np.float64)))
+                w = w.to(dev)
+        return pts, w
+
+    def _weight_plan(self, w: torch.Tensor | None, n: int) -> _WeightPlan:
+        if w is None:
+            return _WeightPlan(0, True, 1.0)
+        out = torch.empty(3, dtype=torch.int64, device=self.device)
+        N.call("gp_weight_probe", w.data_ptr(), n, out.data_ptr(), self.sh)
+        flags, low, mx_bits = (int(v) for v in out.cpu().tolist())
+        mx = np.array([mx_bits], dtype=np.int64).view(np.float64)[0]
+        mode = 2 if flags & 2 else 1
+        if flags & 1:
+            return _WeightPlan(2, False, 1.0)
+        s = max(0, -low) if low < 4096 else 0
+        exact = (s <= 1000 and mx * 2.0 ** s * n < 2.0 ** 53)
+        return _WeightPlan(mode, bool(exact), 2.0 ** s if exact else 1.0)
+
+    def bootstrap(self, points, weights):
+        st = self.settings
+        pts, w = self._input(points, weights)
+        n, d = pts.shape
+        self.n, self.d = n, d
+        k = st.k
+        if k > n:
+            raise ValueError(f"k={k} exceeds the number of points {n}")
+        depth = st.sfc_depth if st.sfc_depth is not None else DEFAULT_DEPTH.get(d)
+        if depth is None or d not in (2, 3):
+            raise GeometryError(f"unsupported dimension {d}")
+        if d * depth > 62:
+            raise GeometryError(f"depth {depth} out of range for dimension {d}")
+        dev, sh = self.device, self.sh
+        sp, sd = pts.stride()
+        # K1: global box (kmeans.py:546-548)
+        lohi = torch.empty(2 * d, dtype=torch.float64, device=dev)
+        bad = torch.empty(1, dtype=torch.int32, device=dev)
+        N.call("gp_box_minmax", pts.data_ptr(), n, d, sp, sd, lohi.data_ptr(), bad.data_ptr(), sh)
+        lohi_h = lohi.cpu().numpy()
+        if int(bad.item()):
+            raise GeometryError("non-finite box corner")
+        self.box = BoundingBox(lohi_h[:d].copy(), lohi_h[d:].copy())
+        # weights plan
+        self.wplan = self._weight_plan(w, n)
+        # K2 keys + K3 sort + payload gather (geometry.py:182, ranksim.py:143-170)
+        keys = torch.empty(n, dtype=torch.int64, device=dev)
+        gids = torch.empty(n, dtype=torch.int32, device=dev)
+        N.call("gp_hilbert_keys", pts.data_ptr(), n, d, sp, sd, lohi.data_ptr(), depth,
+               keys.data_ptr(), gids.data_ptr(), 0, sh)
+        keys_s = torch.empty_like(keys)
+        self.gids = torch.empty_like(gids)
+        wsb = N.size_query("gp_sort_workspace_bytes", n)
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        N.call("gp_sort_pairs", keys.data_ptr(), gids.data_ptr(), keys_s.data_ptr(),
+               self.gids.data_ptr(), n, d * depth, ws.data_ptr(), wsb, sh)
+        self.keys_sorted = keys_s
+        del keys, gids, ws
+        self.ldx = n
+        self.X = torch.empty((d, n), dtype=torch.float64, device=dev)
+        self.W = None
+        if w is not None:
+            self.W = torch.empty(n, dtype=torch.float32 if self.wplan.mode == 1 else torch.float64,
+                                 device=dev)
+        N.call("gp_gather_points", pts.data_ptr(), sp, sd, d, self.gids.data_ptr(), n,
+               self.X.data_ptr(), self.ldx, _ptr(w), self.wplan.mode if w is not None else 0,
+               _ptr(self.W), sh)
+        # K4 initial centers (kmeans.py:552-558)
+        pos = torch.from_numpy(initial_center_positions(n, k)).to(dev)
+        cen = torch.empty((k, d), dtype=torch.float64, device=dev)
+        N.call("gp_gather_rows", self.X.data_ptr(), self.ldx, d, pos.data_ptr(), k,
+               cen.data_ptr(), sh)
+        self.centers_d = cen
+        self.init_centers = cen.cpu().numpy().copy()
+        # sample ranks in SFC order (kmeans.py:564-568)
+        self.sizes = sample_schedule(n, st.init_sample)
+        if self.sizes:
+            perm = np.random.default_rng(st.seed).permutation(n)
+            rank = np.empty(n, dtype=np.int32)
+            rank[perm] = np.arange(n, dtype=np.int32)
+            rank_d = torch.from_numpy(rank).to(dev)
+            self.rank_sfc = torch.empty(n, dtype=torch.int32, device=dev)
+            N.call("gp_gather_ranks", rank_d.data_ptr(), self.gids.data_ptr(), n,
+                   self.rank_sfc.data_ptr(), sh)
+            cwb = N.size_query("gp_compact_workspace_bytes", n)
+            self.compact_ws = torch.empty(max(cwb, 8), dtype=torch.uint8, device=dev)
+            self.active_idx = torch.empty(n, dtype=torch.int32, device=dev)
+            self.active_cnt = torch.empty(1, dtype=torch.int64, device=dev)
+        return self
+
+    # ------------------------------------------------------------ helpers
+    def _alloc_state(self):
+        n, k, d, dev = self.n, self.settings.k, self.d, self.device
+        self.A = torch.full((n,), -1, dtype=torch.int32, device=dev)
+        self.UB = torch.full((n,), math.inf, dtype=torch.float64, device=dev)
+        self.LB = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.kstate = torch.empty(3 * k, dtype=torch.float64, device=dev)  # infl | ubS | ubT
+        self.red = torch.zeros(k + 3, dtype=torch.int64, device=dev)      # block_w | counters
+        self.audit_out = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.fold_out = torch.empty(k * (d + 3), dtype=torch.float64, device=dev)
+        fwb = N.size_query("gp_fold_workspace_bytes", n, 0, n, k)
+        self.fold_ws = torch.empty(max(fwb, 8), dtype=torch.uint8, device=dev)
+        a = N.AssignArgs()
+        a.X, a.ldx, a.d, a.k, a.order3 = self.X.data_ptr(), self.ldx, d, k, self.order3
+        a.wmode = self.wplan.mode if self.W is not None else 0
+        a.w = _ptr(self.W)
+        a.wscale = self.wplan.scale
+        a.a, a.ub, a.lb = self.A.data_ptr(), self.UB.data_ptr(), self.LB.data_ptr()
+        a.centers = self.centers_d.data_ptr()
+        base = self.kstate.data_ptr()
+        a.infl, a.ub_scale, a.ub_shift = base, base + 8 * k, base + 16 * k
+        a.block_w = self.red.data_ptr()
+        a.counters = self.red.data_ptr() + 8 * k
+        self.aargs = a
+        f = N.FoldArgs()
+        f.X, f.ldx, f.d, f.k, f.order3 = self.X.data_ptr(), self.ldx, d, k, self.order3
+        f.wmode, f.w, f.a = a.wmode, a.w, self.A.data_ptr()
+        f.n_local, f.pos0, f.n_global = n, 0, n
+        f.centers = self.centers_d.data_ptr()
+        fo = self.fold_out.data_ptr()
+        f.sums, f.wsum, f.extent, f.objective = fo, fo + 8 * k * d, fo + 8 * k * (d + 1), \
+            fo + 8 * k * (d + 2)
+        f.workspace, f.workspace_bytes = self.fold_ws.data_ptr(), self.fold_ws.numel()
+        self.fargs = f
+
+    def _push_kstate(self, infl, maps: BoundMaps):
+        k = self.settings.k
+        host = np.concatenate([infl, maps.ub_scale, maps.ub_shift])
+        self.kstate.copy_(torch.from_numpy(host), non_blocking=False)
+        self.aargs.lb_scale = maps.lb_scale
+        self.aargs.lb_shift = maps.lb_shift
+        self.aargs.bound_err = maps.bound_err
+        del k
+
+    def _set_active(self, size):
+        a = self.aargs
+        if size is None:
+            a.list, a.m = None, self.n
+            return self.n
+        N.call("gp_compact_active", self.rank_sfc.data_ptr(), self.n, size,
+               self.active_idx.data_ptr(), self.active_cnt.data_ptr(),
+               self.compact_ws.data_ptr(), self.compact_ws.numel(), self.sh)
+        m = int(self.active_cnt.item())
+        a.list, a.m = self.active_idx.data_ptr(), m
+        return m
+
+    def _assign(self):
+        self.red.zero_()
+        if self.timer is not None:
+            e0 = self.timer.mark(self.stream)
+        N.count("gp_assign_round")
+        N.check(N.lib.gp_assign_round(C.byref(self.aargs), self.sh), "gp_assign_round")
+        if self.timer is not None:
+            self.timer.events.append((e0, self.timer.mark(self.stream)))
+        host = self.red.cpu().numpy()
+        k = self.settings.k
+        cnt = host[k:k + 3]
+        if self.timer is not None:
+            self.timer.rounds.append((int(cnt[1]), int(cnt[1] - cnt[0]), int(cnt[2])))
+        return host[:k], cnt
+
+    def _block_weights(self, blk_int):
+        if self.wplan.exact:
+            return blk_int.astype(np.float64) / self.wplan.scale
+        f = self.fargs
+        f.weights_only = 1
+        N.count("gp_movement_fold")
+        N.check(N.lib.gp_movement_fold(C.byref(f), self.sh), "gp_movement_fold")
+        k = self.settings.k
+        return self.fold_out[k * self.d:k * (self.d + 1)].cpu().numpy().copy()
+
+    # ------------------------------------------------------------ main loop
+    def run(self):
+        st, n, d, k = self.settings, self.n, self.d, self.settings.k
+        self._alloc_state()
+        centers = self.init_centers.copy()
+        infl = np.ones(k)
+        block_w = np.zeros(k)
+        last_move = np.zeros(k)
+        maps = BoundMaps(k)
+        self._push_kstate(infl, maps)
+        threshold = st.delta_threshold
+        if threshold is None:
+            threshold = 1e-4 * self.box.diagonal()
+        stats = KMeansStats()
+        plan = [("sample", s) for s in self.sizes] + [("full", None)] * st.max_iter
+        info = None
+        fallback = None
+        scale_hint = max(self.box.diagonal(), 1e-300)
+        for step, (phase, size) in enumerate(plan):
+            m = self._set_active(size)
+            # ---------------- assign_and_balance (kmeans.py:377-453)
+            skips = decisions = evals = 0
+            final_imb = math.inf
+            best_imb = math.inf
+            cap = st.influence_step_cap
+            regressions = 0
+            history = []
+            rounds = 0
+            for rnd in range(st.max_balance_iter):
+                rounds += 1
+                if st.audit_bounds:
+                    N.count("gp_audit")
+                    N.check(N.lib.gp_audit(C.byref(self.aargs), self.audit_out.data_ptr(), self.sh),
+                            "gp_audit")
+                blk, cnt = self._assign()
+                skips += int(cnt[0])
+                decisions += int(cnt[1])
+                evals += int(cnt[2])
+                block_w = self._block_weights(blk)
+                final_imb = imbalance(block_w)
+                history.append(final_imb)
+                if final_imb <= st.epsilon or rnd == st.max_balance_iter - 1:
+                    break
+                if final_imb > best_imb:
+                    regressions += 1
+                    if regressions >= 2:
+                        cap *= 0.5
+                best_imb = min(best_imb, final_imb)
+                target = float(block_w.sum()) / k
+                if not target > 0:
+                    raise ValueError("target weight must be positive")
+                new_infl = infl * influence_factor(block_w, target, cap, d)
+                maps.relax(infl, new_infl, np.zeros(k))
+                infl = new_infl
+                self._push_kstate(infl, maps)
+            info = BalanceInfo(rounds, final_imb, block_w, skips, decisions, evals, history)
+            if phase == "full" and info.imbalance <= st.epsilon:
+                if fallback is None:
+                    self.A_fb = torch.empty_like(self.A)
+                self.A_fb.copy_(self.A)
+                fallback = (ClusterState(centers.copy(), infl.copy(), block_w.copy(),
+                                         last_move.copy()), info.imbalance)
+            # ---------------- movement (kmeans.py:585-626)
+            f = self.fargs
+            f.weights_only = 0
+            N.count("gp_movement_fold")
+            N.check(N.lib.gp_movement_fold(C.byref(f), self.sh), "gp_movement_fold")
+            red = self.fold_out.cpu().numpy()
+            sums = red[:k * d].reshape(k, d)
+            totals = red[k * d:k * (d + 1)]
+            extents = red[k * (d + 1):k * (d + 2)]
+            obj_parts = red[k * (d + 2):k * (d + 3)]
+            empty = totals == 0
+            safe = np.where(empty, 1.0, totals)
+            new_centers = sums / safe[:, None]
+            new_centers[empty] = centers[empty]
+            moves = np.linalg.norm(new_centers - centers, axis=1)
+            stats.iterations.append(IterationRecord(
+                phase=phase, active_points=m, balance_rounds=info.rounds,
+                imbalance=info.imbalance, skip_decisions=info.skip_decisions,
+                total_decisions=info.total_decisions, distance_evals=info.distance_evals,
+                objective=float(obj_parts.sum()), max_move=float(moves.max())))
+            last = step == len(plan) - 1
+            converged = phase == "full" and float(moves.max()) < threshold
+            if converged or last:
+                stats.converged = converged
+                break
+            old_infl = infl
+            nxt = old_infl * np.where(empty, 1.0 + st.influence_step_cap, 1.0)
+            if st.erosion:
+                nonempty = block_w > 0
+                beta = float(2.0 * extents[nonempty].mean()) if nonempty.any() else 0.0
+                if beta > 0:
+                    nxt = eroded(nxt, moves, beta)
+            maps.relax(old_infl, nxt, moves)
+            centers = new_centers
+            infl = nxt
+            last_move = moves
+            self.centers_d.copy_(torch.from_numpy(np.ascontiguousarray(centers)))
+            if maps.needs_rebase(scale_hint / max(float(infl.min()), 1e-300)):
+                self._push_kstate(infl, maps)
+                a = self.aargs
+                lst, mm = a.list, a.m
+                a.list, a.m = None, n
+                N.count("gp_rebase_bounds")
+                N.check(N.lib.gp_rebase_bounds(C.byref(a), self.sh), "gp_rebase_bounds")
+                a.list, a.m = lst, mm
+                maps.reset()
+            self._push_kstate(infl, maps)
+
+        final_state = ClusterState(centers, infl, block_w, last_move)
+        final_imb = info.imbalance
+        A = self.A
+        if final_imb > st.epsilon and fallback is not None:
+            A = self.A_fb
+            final_state, final_imb = fallback
+        stats.balance_failed = final_imb > st.epsilon
+        stats.final_state = final_state
+        if st.audit_bounds:
+            aud = self.audit_out.cpu().numpy()
+            stats.audited_point_iterations = int(aud[0])
+            stats.bound_violations = int(aud[1])
+            stats.skip_check_failures = int(aud[2])
+        out = torch.empty(n, dtype=torch.int64, device=self.device)
+        N.call("gp_scatter_by_gid", A.data_ptr(), self.gids.data_ptr(), n, out.data_ptr(), self.sh)
+        return out, stats
+
+
+def partition_device(points, weights, settings: KMeansSettings, device=None, timer=None):
+    """Run on one GPU; returns (device int64 assignment by original id, KMeansStats)."""
+    eng = DevicePartitioner(settings, device=device, timer=timer)
+    eng.bootstrap(points, weights)
+    return eng.run()
+
+
+def _finish(assign_dev, stats, k, return_stats):
+    assignment = assign_dev.cpu().numpy()
+    part = Partition(assignment=assignment, k=k, balance_failed=stats.balance_failed,
+                     empty_blocks=np.flatnonzero(stats.final_state.block_weights == 0))
+    return (part, stats) if return_stats else part
+
+
+def balanced_kmeans_points(points, weights, settings: KMeansSettings, p: int = 1,
+                           return_stats: bool = False):
+    """Partition a raw point set (kmeans.py:502-512); identical results for every p."""
+    if not isinstance(points, torch.Tensor):
+        points = np.asarray(points, dtype=np.float64)
+    RankWorld.from_points(points, weights, p)  # rank-count validation (ranksim.py:98-100)
+    assign_dev, stats = partition_device(points, weights, settings)
+    return _finish(assign_dev, stats, settings.k, return_stats)
+
+
+def balanced_kmeans(graph, settings: KMeansSettings, world: RankWorld | None = None,
+                    return_stats: bool = False):
+    """Partition a geometric graph's vertices (kmeans.py:515-534)."""
+    if world is None:
+        world = RankWorld.from_graph(graph)
+    elif world.n != graph.n:
+        raise ValueError("world does not match the graph")
+    assign_dev, stats = partition_device(graph.coords, graph.vertex_weights, settings)
+    return _finish(assign_dev, stats, settings.k, return_stats)
