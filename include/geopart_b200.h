@@ -125,8 +125,35 @@ typedef struct gp_assign_args {
   unsigned long long* counters; /* out: [skips, decisions, evals], accumulated */
   double bound_err;       /* relative error bound of the host-composed maps: evaluated
                              bounds are widened by bound_err * (|scale*b~| + |shift|) */
+  /* optional hierarchical candidate source (gp_group_candidates): entry li of
+   * the active list belongs to group li >> group_shift, whose candidate centers
+   * are group_list[g*group_cap .. +group_count[g]); group_count[g] < 0 means
+   * "all k".  NULL group_list: every tile starts from all k centers. */
+  const int32_t* group_list;
+  const int32_t* group_count;
+  int32_t group_cap;
+  int32_t group_shift;
 } gp_assign_args;
 int gp_assign_round(const gp_assign_args* args, void* stream);
+
+/* Hierarchical candidate lists (a B200 replacement for the reference's one
+ * box per rank, kmeans.py:315-319).  Entries of the active list are grouped in
+ * aligned runs of 2^shift (SFC-contiguous, so each group is spatially
+ * compact).
+ *  gp_group_boxes: per group the bounding box of its points, boxes[g*2d ..]
+ *    = (lo[0..d), hi[0..d)); computed once per active set.
+ *  gp_group_candidates: per group, every center whose box lower bound does not
+ *    exceed the second smallest box upper bound (a sound superset of each
+ *    member point's best and runner-up center under the current influences),
+ *    taken from the parent level's list (parent_list/parent_count with
+ *    parent_shift >= shift) or from all k when parent_list is NULL.  A group
+ *    whose list would exceed cap gets count -1 ("all k"). */
+int gp_group_boxes(const double* X, int64_t ldx, int d, const int32_t* list, int64_t m,
+                   int shift, double* boxes, void* stream);
+int gp_group_candidates(const double* boxes, int64_t ngroups, int d, int k,
+                        const double* centers, const double* infl, const int32_t* parent_list,
+                        const int32_t* parent_count, int parent_cap, int parent_ratio_log2,
+                        int32_t* list, int32_t* count, int cap, void* stream);
 
 /* Re-express every bound under identity maps (when the host's cumulative
  * maps drift out of range).  Same bound semantics as gp_assign_args. */

@@ -100,10 +100,16 @@ __global__ void fold_pairs(const int32_t* __restrict__ first, const int32_t* __r
   }
 }
 
+// One warp per (segment, block) pair.  The span [first, last] is walked in
+// batches of FB chunks of 32 positions: every load of a batch is issued before
+// any of its values is consumed (one memory latency per batch instead of one
+// per chunk), then lane j folds column j over the matched positions in order.
+constexpr int FB = 4;
+
 template <int D>
 __global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const Pair* __restrict__ pairs,
                                                   int64_t* counters, double* out) {
-  __shared__ double sm[FT / 32][MAXCOL][33];
+  __shared__ double sm[FT / 32][MAXCOL][FB * 32 + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ncols = f.weights_only ? 1 : D + 2;
   const int64_t npairs = counters[0];
@@ -112,47 +118,65 @@ __global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const Pair* __
     if (lane == 0) pi = (int64_t)atomicAdd((unsigned long long*)&counters[1], 1ull);
     pi = __shfl_sync(FULL, pi, 0);
     if (pi >= npairs) break;
-    Pair pr = pairs[pi];
+    const Pair pr = pairs[pi];
     const int c = pr.key % f.k;
     double cold[D];
     if (!f.weights_only) {
 #pragma unroll
       for (int j = 0; j < D; ++j) cold[j] = f.centers[c * D + j];
     }
-    double acc = 0.0;   // lane j < ncols folds column j (bincount starts from 0.0)
+    double acc = 0.0;  // lane j < ncols folds column j; bincount starts from 0.0
     double ext = 0.0;
-    for (int64_t base = pr.first; base <= pr.last; base += 32) {
-      int64_t i = base + lane;
-      bool valid = i <= pr.last && f.a[i] == c;
-      if (valid) {
-        double w = load_weight(f.w, f.wmode, i);
-        if (f.weights_only) {
-          sm[warp][0][lane] = w;
-        } else {
-          double x[D], diff[D];
+    for (int64_t base = pr.first; base <= pr.last; base += FB * 32) {
+      int av[FB];
+      double xv[FB][D], wv[FB];
 #pragma unroll
-          for (int j = 0; j < D; ++j) {
-            x[j] = f.X[j * f.ldx + i];
-            sm[warp][j][lane] = __dmul_rn(x[j], w);  // wx = points * weights[:, None]
-            diff[j] = __dsub_rn(x[j], cold[j]);
-          }
-          double sq = sqnorm_rn(diff, D, f.order3);
-          sm[warp][D][lane] = w;
-          sm[warp][D + 1][lane] = __dmul_rn(sq, w);
-          ext = fmax(ext, __dsqrt_rn(sq));
+      for (int b = 0; b < FB; ++b) {
+        int64_t i = base + b * 32 + lane;
+        bool in = i <= pr.last;
+        av[b] = in ? f.a[i] : -1;
+        wv[b] = in ? load_weight(f.w, f.wmode, i) : 0.0;
+        if (!f.weights_only) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) xv[b][j] = in ? f.X[j * f.ldx + i] : 0.0;
         }
       }
-      unsigned m = __ballot_sync(FULL, valid);
+      unsigned masks[FB];
+#pragma unroll
+      for (int b = 0; b < FB; ++b) {
+        bool valid = av[b] == c;
+        masks[b] = __ballot_sync(FULL, valid);
+        const int slot = b * 32 + lane;
+        if (f.weights_only) {
+          sm[warp][0][slot] = wv[b];
+        } else {
+          double diff[D];
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            sm[warp][j][slot] = __dmul_rn(xv[b][j], wv[b]);  // wx = points * weights[:, None]
+            diff[j] = __dsub_rn(xv[b][j], cold[j]);
+          }
+          double sq = sqnorm_rn(diff, D, f.order3);
+          sm[warp][D][slot] = wv[b];
+          sm[warp][D + 1][slot] = __dmul_rn(sq, wv[b]);
+          if (valid) ext = fmax(ext, __dsqrt_rn(sq));
+        }
+      }
       __syncwarp();
       if (lane < ncols) {
-        if (m == FULL) {
+        const double* col = sm[warp][lane];
 #pragma unroll
-          for (int b = 0; b < 32; ++b) acc = __dadd_rn(acc, sm[warp][lane][b]);
-        } else {
-          while (m) {
-            int b = __ffs(m) - 1;
-            m &= m - 1;
-            acc = __dadd_rn(acc, sm[warp][lane][b]);
+        for (int b = 0; b < FB; ++b) {
+          unsigned m = masks[b];
+          if (m == FULL) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) acc = __dadd_rn(acc, col[b * 32 + t]);
+          } else {
+            while (m) {
+              int t = __ffs(m) - 1;
+              m &= m - 1;
+              acc = __dadd_rn(acc, col[b * 32 + t]);
+            }
           }
         }
       }
@@ -165,38 +189,49 @@ __global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const Pair* __
   }
 }
 
+// One warp per block: gather the block's pair partials over the segments
+// (independent loads), then fold them in segment order (np.add.reduce(axis=0)).
 template <int D>
 __global__ void fold_combine(gp_fold_args f, const int32_t* __restrict__ slot, int64_t nseg,
                              const double* __restrict__ out) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ int32_t s_slot[4][GP_SEGMENTS];
+  __shared__ int s_cnt[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 4 + warp;
   if (c >= f.k) return;
-  if (f.weights_only) {
-    double w = 0.0;
-    for (int64_t s = 0; s < nseg; ++s) {
-      int32_t p = slot[s * f.k + c];
-      if (p >= 0) w = __dadd_rn(w, out[(int64_t)p * (MAXCOL + 1)]);
-    }
-    f.wsum[c] = w;
-    return;
+  // ordered compaction of the present segments
+  if (lane == 0) s_cnt[warp] = 0;
+  __syncwarp();
+  int base = 0;
+  for (int64_t s0 = 0; s0 < nseg; s0 += 32) {
+    int64_t s = s0 + lane;
+    int32_t p = s < nseg ? slot[s * f.k + c] : -1;
+    unsigned m = __ballot_sync(FULL, p >= 0);
+    if (p >= 0) s_slot[warp][base + __popc(m & ((1u << lane) - 1))] = p;
+    base += __popc(m);
   }
-  double acc[D + 2];
-#pragma unroll
-  for (int j = 0; j < D + 2; ++j) acc[j] = 0.0;
-  double ext = 0.0;
-  for (int64_t s = 0; s < nseg; ++s) {
-    int32_t p = slot[s * f.k + c];
-    if (p >= 0) {
-      const double* po = out + (int64_t)p * (MAXCOL + 1);
-#pragma unroll
-      for (int j = 0; j < D + 2; ++j) acc[j] = __dadd_rn(acc[j], po[j]);
-      ext = fmax(ext, po[MAXCOL]);
+  __syncwarp();
+  const int np = base;
+  const int ncols = f.weights_only ? 1 : D + 2;
+  if (lane < ncols) {
+    double acc = 0.0;
+    for (int i = 0; i < np; ++i) acc = __dadd_rn(acc, out[(int64_t)s_slot[warp][i] * (MAXCOL + 1) + lane]);
+    if (f.weights_only) {
+      f.wsum[c] = acc;
+    } else if (lane < D) {
+      f.sums[c * D + lane] = acc;
+    } else if (lane == D) {
+      f.wsum[c] = acc;
+    } else {
+      f.objective[c] = acc;
     }
   }
-#pragma unroll
-  for (int j = 0; j < D; ++j) f.sums[c * D + j] = acc[j];
-  f.wsum[c] = acc[D];
-  f.objective[c] = acc[D + 1];
-  f.extent[c] = ext;
+  if (!f.weights_only) {
+    double ext = 0.0;
+    for (int i = lane; i < np; i += 32) ext = fmax(ext, out[(int64_t)s_slot[warp][i] * (MAXCOL + 1) + MAXCOL]);
+    for (int o = 16; o; o >>= 1) ext = fmax(ext, __shfl_xor_sync(FULL, ext, o));
+    if (lane == 0) f.extent[c] = ext;
+  }
 }
 
 }  // namespace gp
@@ -243,10 +278,10 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
                                                              counters);
   if (f->d == 2) {
     fold_kernel<2><<<sms * 8, FT, 0, s>>>(*f, pairs, counters, out);
-    fold_combine<2><<<grid_for(f->k, 128), 128, 0, s>>>(*f, slot, L.nseg, out);
+    fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   } else {
     fold_kernel<3><<<sms * 8, FT, 0, s>>>(*f, pairs, counters, out);
-    fold_combine<3><<<grid_for(f->k, 128), 128, 0, s>>>(*f, slot, L.nseg, out);
+    fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   }
   return check_launch("movement_fold");
 }

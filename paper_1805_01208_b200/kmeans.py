@@ -110,6 +110,62 @@ class _Timer:
         return sum(a.elapsed_time(b) for a, b in self.events)
 
 
+class _Hierarchy:
+    """Group-level candidate lists (gp_group_boxes / gp_group_candidates).
+
+    Super groups of 2^15 active entries take their candidates from mega groups
+    of 2^20 entries (k > 4096) or from all k; tiles of the assign kernel then
+    start from their super group's list instead of all k centers.
+    """
+
+    SUPER_SHIFT, MEGA_SHIFT = 15, 20
+    SUPER_CAP, MEGA_CAP = 1024, 4096
+
+    def __init__(self, eng, use_mega: bool):
+        self.eng = eng
+        self.use_mega = use_mega
+        self.key = None
+
+    def prepare(self, list_ptr, m):
+        """Boxes of the groups of the current active list (once per active set)."""
+        eng = self.eng
+        if self.key == (list_ptr, m):
+            return
+        self.key = (list_ptr, m)
+        dev, d = eng.device, eng.d
+        self.ns = max(1, (m + (1 << self.SUPER_SHIFT) - 1) >> self.SUPER_SHIFT)
+        self.nm = max(1, (m + (1 << self.MEGA_SHIFT) - 1) >> self.MEGA_SHIFT)
+        self.sbox = torch.empty(self.ns * 2 * d, dtype=torch.float64, device=dev)
+        self.slist = torch.empty(self.ns * self.SUPER_CAP, dtype=torch.int32, device=dev)
+        self.scount = torch.empty(self.ns, dtype=torch.int32, device=dev)
+        N.call("gp_group_boxes", eng.X.data_ptr(), eng.ldx, d, list_ptr, m, self.SUPER_SHIFT,
+               self.sbox.data_ptr(), eng.sh)
+        if self.use_mega:
+            self.mbox = torch.empty(self.nm * 2 * d, dtype=torch.float64, device=dev)
+            self.mlist = torch.empty(self.nm * self.MEGA_CAP, dtype=torch.int32, device=dev)
+            self.mcount = torch.empty(self.nm, dtype=torch.int32, device=dev)
+            N.call("gp_group_boxes", eng.X.data_ptr(), eng.ldx, d, list_ptr, m,
+                   self.MEGA_SHIFT, self.mbox.data_ptr(), eng.sh)
+        a = eng.aargs
+        a.group_list, a.group_count = self.slist.data_ptr(), self.scount.data_ptr()
+        a.group_cap, a.group_shift = self.SUPER_CAP, self.SUPER_SHIFT
+
+    def refresh(self):
+        """Candidate lists under the current centers and influences (every round)."""
+        eng = self.eng
+        d, k = eng.d, eng.settings.k
+        cen, infl = eng.centers_d.data_ptr(), eng.kstate.data_ptr()
+        parent, pcount, pcap = None, None, 0
+        if self.use_mega:
+            N.call("gp_group_candidates", self.mbox.data_ptr(), self.nm, d, k, cen, infl,
+                   None, None, 0, 0, self.mlist.data_ptr(), self.mcount.data_ptr(),
+                   self.MEGA_CAP, eng.sh)
+            parent, pcount, pcap = self.mlist.data_ptr(), self.mcount.data_ptr(), self.MEGA_CAP
+        N.call("gp_group_candidates", self.sbox.data_ptr(), self.ns, d, k, cen, infl,
+               parent, pcount, pcap, self.MEGA_SHIFT - self.SUPER_SHIFT,
+               self.slist.data_ptr(), self.scount.data_ptr(), self.SUPER_CAP, eng.sh)
+
+
 class DevicePartitioner:
     """One partition run on one GPU (the whole point set is one SFC shard)."""
 
@@ -248,6 +304,7 @@ class DevicePartitioner:
         a.block_w = self.red.data_ptr()
         a.counters = self.red.data_ptr() + 8 * k
         self.aargs = a
+        self.hier = _Hierarchy(self, use_mega=k > 4096) if k > 128 else None
         f = N.FoldArgs()
         f.X, f.ldx, f.d, f.k, f.order3 = self.X.data_ptr(), self.ldx, d, k, self.order3
         f.wmode, f.w, f.a = a.wmode, a.w, self.A.data_ptr()
@@ -269,6 +326,12 @@ class DevicePartitioner:
         del k
 
     def _set_active(self, size):
+        m = self._set_active_list(size)
+        if self.hier is not None:
+            self.hier.prepare(self.aargs.list, m)
+        return m
+
+    def _set_active_list(self, size):
         a = self.aargs
         if size is None:
             a.list, a.m = None, self.n
@@ -281,6 +344,8 @@ class DevicePartitioner:
         return m
 
     def _assign(self):
+        if self.hier is not None:
+            self.hier.refresh()
         self.red.zero_()
         if self.timer is not None:
             e0 = self.timer.mark(self.stream)

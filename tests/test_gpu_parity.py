@@ -262,3 +262,39 @@ def test_device_tensor_inputs_give_same_result():
     b = balanced_kmeans_points(torch.from_numpy(pts).cuda(), torch.from_numpy(w).cuda(),
                                s).assignment
     assert np.array_equal(a, b)
+
+
+# ------------------------------------------------ hierarchical candidate lists
+@pytest.mark.parametrize("recipe", ["c3_small", "c4_small"])
+def test_scaled_down_3d_configs_vs_oracle(recipe):
+    """C3/C4 recipes at 2^18 points (k=256, several candidate groups) vs the oracle."""
+    from paper_1805_01208_b200.workloads import c3, c4
+
+    O = _oracle()
+    if recipe == "c3_small":
+        pts, w = c3(seed=1, side=64)
+        k, eps = 256, 0.03
+    else:
+        pts, w = c4(seed=1, n=1 << 18)
+        k, eps = 256, 0.05
+    s = KMeansSettings(k=k, epsilon=eps, seed=0, max_iter=6)
+    part, stats = balanced_kmeans_points(pts, w, s, return_stats=True)
+    r = O.run(pts, w, O.Knobs(k=k, epsilon=eps, seed=0, max_iter=6), scan_chunks=256)
+    assert np.array_equal(part.assignment, r.assignment)
+    assert np.array_equal(stats.final_state.centers, r.centers)
+    assert np.array_equal(stats.final_state.influence, r.influence)
+    _compare_records(stats.iterations, r.records)
+
+
+def test_large_k_mega_level_exact_argmin():
+    """k > 4096 exercises the mega -> super -> tile candidate hierarchy."""
+    O = _oracle()
+    rng = np.random.default_rng(21)
+    pts = rng.random((200_000, 2))
+    pts[:50_000] = 0.5 + 0.05 * rng.standard_normal((50_000, 2))
+    s = KMeansSettings(k=5000, seed=0, max_iter=2, max_balance_iter=3)
+    part, stats = balanced_kmeans_points(pts, None, s, return_stats=True)
+    st = stats.final_state
+    assert np.array_equal(part.assignment, O.brute_labels(pts, st.centers, st.influence))
+    assert sum(r.distance_evals for r in stats.iterations) < 0.05 * sum(
+        r.total_decisions for r in stats.iterations) * 5000
