@@ -77,10 +77,50 @@ def workload(cfg):
     return c, pts, w
 
 
+def device_workload(cfg, dev):
+    """(config, points (n,d) device view, weights or None, host-array getter)."""
+    import torch
+
+    from paper_1805_01208_b200.workloads import CONFIGS, c5_device
+
+    c = CONFIGS[cfg]
+    if cfg == "C5":
+        X = c5_device(n=c["n"], seed=0, device=dev)       # (2, n) SoA
+        pts_d = X.t()                                       # (n, 2) view, strides (1, n)
+
+        def host():
+            h = torch.empty((c["n"], 2), dtype=torch.float64, pin_memory=True)
+            for j in range(2):
+                h[:, j].copy_(X[j])
+            return h.numpy(), None
+        return c, pts_d, None, host
+    _, pts, w = workload(cfg)
+    pts_d = torch.from_numpy(pts).to(dev)
+    w_d = None if w is None else torch.from_numpy(w).to(dev)
+    return c, pts_d, w_d, (lambda: (pts, w))
+
+
+def cpu_inputs(cfg):
+    """Bounded CPU-baseline input: the config itself, or for C5 (16 GiB, days on the
+    reference) the same recipe at 2^21 points with k scaled to keep 65536/16 points
+    per block... see the 'sample' string."""
+    from paper_1805_01208_b200.workloads import CONFIGS, c5_host
+
+    if cfg == "C5":
+        n = 1 << 21
+        c = dict(CONFIGS["C5"], n=n, k=512)
+        pts, w = c5_host(seed=0, n=n)
+        return c, pts, w, "C5 recipe at n=2^21 (1/512 of the points), k=512"
+    c, pts, w = workload(cfg)
+    return c, pts, w, f"{cfg} input"
+
+
 # ------------------------------------------------------------ CPU (oracle) arm
-def cpu_sample(cfg, c, pts, w, budget_s=25.0):
+def cpu_sample(cfg, c=None, pts=None, w=None, budget_s=25.0):
     """Oracle on the same input: sample phase + as many full iterations as fit ~budget."""
     from oracle import geographer_oracle as O
+
+    c, pts, w, what = cpu_inputs(cfg)
 
     iters = 1
     t0 = time.perf_counter()
@@ -96,7 +136,7 @@ def cpu_sample(cfg, c, pts, w, budget_s=25.0):
         dt = time.perf_counter() - t0
         dec = sum(rec["total_decisions"] for rec in r.records)
     return dict(value=dec / dt / 1e9, unit="Gpt/s", cores=1, kind="port",
-                sample=f"{cfg} input, full sample phase + {iters} full iteration(s) "
+                sample=f"{what}, full sample phase + {iters} full iteration(s) "
                        f"(max_iter={iters}), oracle numpy single-threaded, 256 scan chunks; "
                        f"{dec} point-assignments in {dt:.2f} s",
                 seconds=dt)
@@ -106,11 +146,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    c, pts, w = workload(args.config)
+    c, pts, w, _ = cpu_inputs(args.config)
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        s = cpu_sample(args.config, c, pts, w, budget_s=10.0)
+        s = cpu_sample(args.config, budget_s=10.0)
         if i >= args.warmup:
             vals.append(s["value"])
             last = s
@@ -120,8 +160,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": last["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SURVEY §8d recipe)",
-        "config": {"workload": f"{args.config}: {DESCR[args.config]}", "n": int(pts.shape[0]),
-                   "d": int(pts.shape[1]), "k": c["k"], "epsilon": c["epsilon"]},
+        "config": {"workload": f"{args.config}: {DESCR[args.config]}", "n": int(c["n"]),
+                   "d": int(c["d"]), "k": c["k"], "epsilon": c["epsilon"]},
         "cpu_baseline": {"value": v, "unit": "Gpt/s", "cores": 1, "kind": "port",
                          "sample": last["sample"]},
         "e2e": {"value": v, "unit": "Gpt/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -193,11 +233,9 @@ def run_b200(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    c, pts, w = workload(args.config)
-    n, d = pts.shape
+    c, pts_d, w_d, host_inputs = device_workload(args.config, dev)
+    n, d = pts_d.shape
     settings = KMeansSettings(k=c["k"], epsilon=c["epsilon"], seed=0)
-    pts_d = torch.from_numpy(pts).to(dev)
-    w_d = None if w is None else torch.from_numpy(w).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     N.reset_launch_count()
 
@@ -243,7 +281,7 @@ def run_b200(args):
     value = decisions / t_total / 1e9
 
     # roofline of the assign kernel
-    wb = 0 if w is None else 8
+    wb = 0 if w_d is None else 8
     alg_bytes, kern_ms, flops = 0.0, 0.0, 0.0
     for timer, stats in timers:
         kern_ms += timer.total_ms()
@@ -257,6 +295,7 @@ def run_b200(args):
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        pts, w = host_inputs()
         e2e_t = []
         for i in range(max(1, min(args.steps, 3)) + 1):
             flush.fill_(1)
@@ -274,7 +313,7 @@ def run_b200(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample(args.config, c, pts, w)
+        cpu = cpu_sample(args.config)
         cpu.pop("seconds", None)
 
     if rank == 0:

@@ -94,6 +94,15 @@ int gp_compact_workspace_bytes(int64_t n, size_t* bytes);
 int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx,
                       int64_t* count, void* workspace, size_t workspace_bytes, void* stream);
 
+/* K5b warm-up sample order, bit-exact with numpy: rank[perm[t]] = t for
+ * perm = numpy.random.default_rng(seed).permutation(n) (kmeans.py:564-567).
+ * pcg_state is a HOST array {state_hi, state_lo, inc_hi, inc_lo} of the
+ * generator's PCG64 state (np.random.PCG64(seed).state).  Synchronises the
+ * stream (its acceptance and reservation loops read back small counters). */
+int gp_sample_ranks_workspace_bytes(int64_t n, size_t* bytes);
+int gp_sample_ranks(const uint64_t* pcg_state, int64_t n, int32_t* rank, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* K6  one assign round over the active points of one shard.  Replaces
  * _scan_rank (kmeans.py:297-344) for every rank, the bound relaxations of
  * kmeans.py:438-443 / :622-625 (applied lazily through per-cluster affine
@@ -133,7 +142,11 @@ typedef struct gp_assign_args {
   const int32_t* group_count;
   int32_t group_cap;
   int32_t group_shift;
+  /* scratch of gp_assign_workspace_bytes(m) bytes (filter -> scan hand-off) */
+  void* workspace;
+  size_t workspace_bytes;
 } gp_assign_args;
+int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);
 
 /* Hierarchical candidate lists (a B200 replacement for the reference's one
@@ -165,7 +178,8 @@ int gp_rebase_bounds(const gp_assign_args* args, void* stream);
  * (ranksim.py:218-222), per-block max distance to the old centers
  * (_cluster_extents, kmeans.py:474-487) and the objective terms
  * (kmeans.py:490-499).  Positions pos0..pos0+n_local-1 of a global sequence of
- * n_global points; points with a < 0 are excluded. */
+ * n_global points; points with a < 0 are excluded.  Synchronises the stream
+ * once (it reads back the number of runs to size the run sort). */
 typedef struct gp_fold_args {
   const double* X;
   int64_t ldx;

@@ -31,6 +31,7 @@ class AssignArgs(C.Structure):
         ("centers", vp), ("infl", vp), ("ub_scale", vp), ("ub_shift", vp), ("lb_scale", f64),
         ("lb_shift", f64), ("block_w", vp), ("counters", vp), ("bound_err", f64),
         ("group_list", vp), ("group_count", vp), ("group_cap", i32), ("group_shift", i32),
+        ("workspace", vp), ("workspace_bytes", sz),
     ]
 
 
@@ -58,6 +59,9 @@ _SIGS = {
     "gp_gather_rows": (C.c_int, [vp, i64, C.c_int, vp, C.c_int, vp, vp]),
     "gp_compact_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_compact_active": (C.c_int, [vp, i64, i64, vp, vp, vp, sz, vp]),
+    "gp_sample_ranks_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_sample_ranks": (C.c_int, [C.POINTER(u64), i64, vp, vp, sz, vp]),
+    "gp_assign_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_assign_round": (C.c_int, [C.POINTER(AssignArgs), vp]),
     "gp_rebase_bounds": (C.c_int, [C.POINTER(AssignArgs), vp]),
     "gp_group_boxes": (C.c_int, [vp, i64, C.c_int, vp, i64, C.c_int, vp, vp]),
@@ -104,9 +108,9 @@ def check(rc: int, what: str = "") -> None:
 KERNELS_PER_CALL = {
     "gp_box_minmax": 2, "gp_weight_probe": 1, "gp_hilbert_keys": 1, "gp_sort_pairs": 9,
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 3,
-    "gp_assign_round": 1, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 5,
+    "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 16,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
-    "gp_group_candidates": 1,
+    "gp_group_candidates": 1, "gp_sample_ranks": 90,
 }
 _launches = [0]
 

@@ -18,8 +18,6 @@
 namespace gp {
 
 constexpr int AT = 256;          // threads per CTA
-constexpr int PPT = 4;           // max entries per thread (runtime ppt in {1,2,4})
-constexpr int TILE_MAX = AT * PPT;
 constexpr int CAP = 512;         // candidate centers staged in shared memory
 constexpr int HSLOTS = 128;      // per-CTA block-weight cache
 constexpr double LO_SLACK = 1.0 - 1e-12;
@@ -91,108 +89,256 @@ __device__ __forceinline__ double qdist(const double* x, const ScanSmem<D>& S, i
   return s * S.i2[i];
 }
 
-template <int D>
-__global__ void __launch_bounds__(AT, 2) assign_kernel(gp_assign_args p, int ppt) {
+// ------------------------------------------------------------ filter kernel
+// Streaming pass over the active entries: skip test with the lazily relaxed
+// bounds (kmeans.py:308-311), exact block weights of the points that keep
+// their assignment, and compaction of the points that must be scanned.
+// Chunk c = entries [c*FCHUNK, (c+1)*FCHUNK); its scanned positions go to
+// scan[c*FCHUNK ..] (no global reservation) and runs[c] = their count.
+// Persistent CTAs walk contiguous chunk ranges (SFC-contiguous, so the
+// per-CTA block-weight cache sees few blocks); each thread owns FPER
+// consecutive entries, loaded with 16-byte vector loads in the full phase.
+constexpr int FTH = 256;
+constexpr int FPER = 8;
+constexpr int FCHUNK = FTH * FPER;   // 2048 entries per chunk
+
+struct AssignLayout {
+  int64_t nchunks;
+  size_t off_list, off_runs, total;
+};
+
+static AssignLayout assign_layout(int64_t m) {
+  AssignLayout L;
+  L.nchunks = (m + FCHUNK - 1) / FCHUNK;
+  if (L.nchunks < 1) L.nchunks = 1;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  size_t o = 0;
+  L.off_list = o; o = al(o + (size_t)L.nchunks * FCHUNK * 4);
+  L.off_runs = o; o = al(o + (size_t)L.nchunks * 4);
+  L.total = o;
+  return L;
+}
+
+// weight in exact integer units of 1/wscale, without fp->int conversions
+// (w * wscale is an integer by construction of wscale = 2^s)
+template <int WM>
+__device__ __forceinline__ long long weight_units(const void* w, int64_t i, int shift) {
+  if (WM == GP_W_UNIT) return 1;
+  if (WM == GP_W_F32) {
+    unsigned b = __float_as_uint(((const float*)w)[i]);
+    int e = (b >> 23) & 0xff;
+    long long mant = e ? ((b & 0x7fffff) | 0x800000) : (b & 0x7fffff);
+    int sh = (e ? e : 1) - 150 + shift;  // value = mant * 2^(e-150) * 2^shift
+    long long v = sh >= 0 ? (mant << sh) : (mant >> -sh);
+    return (b >> 31) ? -v : v;
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong(((const double*)w)[i]);
+  int e = (int)((b >> 52) & 0x7ff);
+  long long mant = e ? (long long)((b & 0xfffffffffffffull) | 0x10000000000000ull)
+                     : (long long)(b & 0xfffffffffffffull);
+  int sh = (e ? e : 1) - 1075 + shift;
+  long long v = sh >= 0 ? (mant << sh) : (mant >> -sh);
+  return (b >> 63) ? -v : v;
+}
+
+template <int WM>
+__global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshift, int64_t nchunks,
+                                                     int32_t* __restrict__ scan,
+                                                     int32_t* __restrict__ runs) {
+  __shared__ int s_ckey[HSLOTS];
+  __shared__ long long s_cval[HSLOTS];
+  __shared__ int s_wcnt[FTH / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < HSLOTS; i += FTH) {
+    s_ckey[i] = -1;
+    s_cval[i] = 0;
+  }
+  __syncthreads();
+  const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const int64_t cb = blockIdx.x * per, ce = min(nchunks, cb + per);
+  unsigned long long nskip = 0;
+  for (int64_t c = cb; c < ce; ++c) {
+    const int64_t e0 = c * FCHUNK + (int64_t)tid * FPER;   // my first entry
+    int a[FPER], q[FPER];
+    double ub[FPER], lb[FPER];
+    if (p.list == nullptr && e0 + FPER <= p.m) {
+      // full phase: positions == entries, 16-byte vector loads
+      const int4* ap = reinterpret_cast<const int4*>(p.a + e0);
+      int4 a0 = ap[0], a1 = ap[1];
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      const double2* up = reinterpret_cast<const double2*>(p.ub + e0);
+      const double2* lp = reinterpret_cast<const double2*>(p.lb + e0);
+#pragma unroll
+      for (int h = 0; h < FPER / 2; ++h) {
+        double2 u = up[h], l = lp[h];
+        ub[2 * h] = u.x; ub[2 * h + 1] = u.y;
+        lb[2 * h] = l.x; lb[2 * h + 1] = l.y;
+      }
+#pragma unroll
+      for (int e = 0; e < FPER; ++e) q[e] = (int)(e0 + e);
+    } else {
+#pragma unroll
+      for (int e = 0; e < FPER; ++e) {
+        const int64_t li = e0 + e;
+        q[e] = li < p.m ? (p.list ? p.list[li] : (int)li) : -1;
+        a[e] = q[e] >= 0 ? p.a[q[e]] : -1;
+        ub[e] = q[e] >= 0 ? p.ub[q[e]] : 0.0;
+        lb[e] = q[e] >= 0 ? p.lb[q[e]] : 0.0;
+      }
+    }
+    // skip test; run-length accumulation of the kept points' weights
+    unsigned need = 0;
+    int run_a = -1;
+    long long run_w = 0;
+    bool broke = false;
+#pragma unroll
+    for (int e = 0; e < FPER; ++e) {
+      if (q[e] < 0) continue;
+      bool skip = false;
+      const int ae = a[e];
+      if (ae >= 0) {
+        const double u = ub_eval(p.ub_scale[ae], ub[e], p.ub_shift[ae], p.bound_err);
+        const double l = lb_eval(p.lb_scale, lb[e], p.lb_shift, p.bound_err);
+        skip = u < l;
+      }
+      if (!skip) {
+        need |= 1u << e;
+        continue;
+      }
+      ++nskip;
+      const long long v = weight_units<WM>(p.w, q[e], wshift);
+      if (ae == run_a) {
+        run_w += v;
+      } else {
+        if (run_a >= 0) {
+          cache_add(s_ckey, s_cval, p.block_w, run_a, run_w);
+          broke = true;
+        }
+        run_a = ae;
+        run_w = v;
+      }
+    }
+    // one warp-wide reduction when every lane ends on the same block (common)
+    const unsigned grp = __match_any_sync(FULL, run_a);
+    const bool uni = grp == FULL && !__any_sync(FULL, broke) && run_a >= 0;
+    if (uni) {
+      long long g = run_w;
+      for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(FULL, g, o);
+      if (lane == 0) cache_add(s_ckey, s_cval, p.block_w, run_a, g);
+    } else if (run_a >= 0) {
+      cache_add(s_ckey, s_cval, p.block_w, run_a, run_w);
+    }
+    // compaction of the points to scan into the chunk's own slots
+    const int mine = __popc(need);
+    int incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wcnt[warp] = incl;
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < FTH / 32; ++w) {
+      const int cw = s_wcnt[w];
+      before += w < warp ? cw : 0;
+      total += cw;
+    }
+    int off = before + incl - mine;
+    int32_t* dst = scan + c * FCHUNK;
+#pragma unroll
+    for (int e = 0; e < FPER; ++e)
+      if (need & (1u << e)) dst[off++] = q[e];
+    if (tid == 0) runs[c] = total;
+    __syncthreads();  // s_wcnt reuse
+  }
+  for (int o = 16; o; o >>= 1) nskip += __shfl_xor_sync(FULL, nskip, o);
+  if (lane == 0 && nskip) atomicAdd(&p.counters[0], nskip);
+  __syncthreads();
+  for (int i = tid; i < HSLOTS; i += FTH)
+    if (s_ckey[i] >= 0 && s_cval[i] != 0)
+      atomicAdd((unsigned long long*)&p.block_w[s_ckey[i]], (unsigned long long)s_cval[i]);
+}
+
+// -------------------------------------------------------------- scan kernel
+// One CTA per filter run: box of the run's points (kmeans.py:315-316, per
+// run), candidate centers (lbnd <= second smallest ubnd over the group's list
+// or all k), then the scan (kmeans.py:326-344) with an approximate prefilter:
+// pass 1 finds the two smallest q = d^2/infl^2; pass 2 evaluates the
+// reference's exact effective distance only where q <= q2 (1 + Q_TOL), a
+// superset of every center whose exact distance is <= the exact runner-up.
+constexpr int SPT = 2;             // points per thread per sub-tile
+constexpr int STILE = AT * SPT;    // 512
+
+template <int D, int WM>
+__global__ void __launch_bounds__(AT, 2) scan_kernel(gp_assign_args p, int wshift, int64_t nchunks,
+                                                     const int32_t* __restrict__ scan,
+                                                     const int32_t* __restrict__ runs) {
   __shared__ ScanSmem<D> S;
-  __shared__ int s_pos[TILE_MAX];     // positions that need a scan
-  __shared__ short s_ent[TILE_MAX];   // their tile-local entry ids
-  __shared__ int s_newa[TILE_MAX];
-  __shared__ unsigned s_scanned[TILE_MAX / 32];
   __shared__ int s_ckey[HSLOTS];
   __shared__ long long s_cval[HSLOTS];
   __shared__ double s_red[2 * D][AT / 32];
   __shared__ double s_two[2][AT / 32];
-  __shared__ int s_nscan, s_ncand;
-  __shared__ unsigned long long s_cnt[3];
-
+  __shared__ int s_ncand;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tile = AT * ppt;
-  const int64_t base = (int64_t)blockIdx.x * tile;
-  if (tid == 0) {
-    s_nscan = 0;
-    s_ncand = 0;
-    s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
-  }
   for (int i = tid; i < HSLOTS; i += AT) {
     s_ckey[i] = -1;
     s_cval[i] = 0;
   }
-  for (int i = tid; i < TILE_MAX / 32; i += AT) s_scanned[i] = 0;
   __syncthreads();
-
-  // ---- 1. skip test with the lazily relaxed bounds (kmeans.py:308-311)
-  int pos[PPT], cur[PPT];
-  double wv[PPT];
-  int nskip = 0, ndec = 0;
-#pragma unroll
-  for (int e = 0; e < PPT; ++e) {
-    pos[e] = -1;
-    cur[e] = -1;
-    wv[e] = 0.0;
-    int ent = e * AT + tid;
-    int64_t li = base + ent;
-    if (e < ppt && li < p.m) {
-      int q = p.list ? p.list[li] : (int)li;
-      pos[e] = q;
-      int a = p.a[q];
-      cur[e] = a;
-      wv[e] = load_weight(p.w, p.wmode, q);
-      ++ndec;
-      bool skip = false;
-      if (a >= 0) {
-        double ub = ub_eval(p.ub_scale[a], p.ub[q], p.ub_shift[a], p.bound_err);
-        double lb = lb_eval(p.lb_scale, p.lb[q], p.lb_shift, p.bound_err);
-        skip = ub < lb;
-      }
-      if (skip) {
-        ++nskip;
-      } else {
-        int slot = atomicAdd(&s_nscan, 1);
-        s_pos[slot] = q;
-        s_ent[slot] = (short)ent;
-        atomicOr(&s_scanned[ent >> 5], 1u << (ent & 31));
-      }
+  unsigned long long nevals = 0;
+  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+  const int cnt = runs[chunk];
+  if (cnt == 0) continue;
+  const int32_t* cscan = scan + chunk * FCHUNK;
+  // candidate source: the group's hierarchical list, or all k centers
+  const int32_t* src = nullptr;
+  int nsrc = p.k;
+  if (p.group_list) {
+    const int64_t g = (chunk * FCHUNK) >> p.group_shift;
+    const int gc = p.group_count[g];
+    if (gc >= 0) {
+      src = p.group_list + g * (int64_t)p.group_cap;
+      nsrc = gc;
     }
   }
-  __syncthreads();
-  const int nscan = s_nscan;
-  unsigned long long nevals = 0;
-
-  if (nscan > 0) {
-    // candidate source: the group's hierarchical list, or all k centers
-    const int32_t* src = nullptr;
-    int nsrc = p.k;
-    if (p.group_list) {
-      int64_t g = base >> p.group_shift;
-      int cnt = p.group_count[g];
-      if (cnt >= 0) {
-        src = p.group_list + g * (int64_t)p.group_cap;
-        nsrc = cnt;
+  for (int t0 = 0; t0 < cnt; t0 += STILE) {
+    const int tn = min(STILE, cnt - t0);
+    __syncthreads();  // previous sub-tile done with s_ncand / S
+    if (tid == 0) s_ncand = 0;
+    int qpos[SPT];
+    double x[SPT][D];
+#pragma unroll
+    for (int r = 0; r < SPT; ++r) {
+      const int s = tid + r * AT;
+      qpos[r] = s < tn ? cscan[t0 + s] : -1;
+      if (qpos[r] >= 0) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[r][j] = p.X[j * p.ldx + qpos[r]];
       }
     }
-    // ---- 2. box of the scanned points (kmeans.py:315-316, per tile)
+    // ---- box of the sub-tile's points
     double lo[D], hi[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       lo[j] = INFINITY;
       hi[j] = -INFINITY;
-    }
-    for (int s = tid; s < nscan; s += AT) {
-      int q = s_pos[s];
 #pragma unroll
-      for (int j = 0; j < D; ++j) {
-        double v = p.X[j * p.ldx + q];
-        lo[j] = fmin(lo[j], v);
-        hi[j] = fmax(hi[j], v);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
+      for (int r = 0; r < SPT; ++r)
+        if (qpos[r] >= 0) {
+          lo[j] = fmin(lo[j], x[r][j]);
+          hi[j] = fmax(hi[j], x[r][j]);
+        }
       for (int o = 16; o; o >>= 1) {
         lo[j] = fmin(lo[j], __shfl_xor_sync(FULL, lo[j], o));
         hi[j] = fmax(hi[j], __shfl_xor_sync(FULL, hi[j], o));
       }
-      if (lane == 0) {
+    }
+    __syncthreads();  // previous sub-tile done with s_red / S
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
         s_red[j][warp] = lo[j];
         s_red[D + j][warp] = hi[j];
       }
@@ -207,16 +353,12 @@ __global__ void __launch_bounds__(AT, 2) assign_kernel(gp_assign_args p, int ppt
         hi[j] = fmax(hi[j], s_red[D + j][w]);
       }
     }
-
-    // ---- 3. candidates: lbnd <= second smallest ubnd over the source
+    // ---- candidates: lbnd <= second smallest ubnd over the source
     double m1 = INFINITY, m2 = INFINITY;
     for (int i = tid; i < nsrc; i += AT) {
-      int c = src ? src[i] : i;
-      double cc[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) cc[j] = p.centers[c * D + j];
+      const int c = src ? src[i] : i;
       double lb_, ub_;
-      box_bounds<D>(cc, lo, hi, p.infl[c], lb_, ub_);
+      box_bounds<D>(p.centers + c * D, lo, hi, p.infl[c], lb_, ub_);
       two_min_merge(m1, m2, ub_, INFINITY);
     }
     for (int o = 16; o; o >>= 1) {
@@ -234,51 +376,33 @@ __global__ void __launch_bounds__(AT, 2) assign_kernel(gp_assign_args p, int ppt
     for (int w = 1; w < AT / 32; ++w) two_min_merge(m1, m2, s_two[0][w], s_two[1][w]);
     const double U = m2;  // +inf when only one center exists
     for (int i = tid; i < nsrc; i += AT) {
-      int c = src ? src[i] : i;
-      double cc[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) cc[j] = p.centers[c * D + j];
+      const int c = src ? src[i] : i;
       double lb_, ub_;
-      box_bounds<D>(cc, lo, hi, p.infl[c], lb_, ub_);
+      box_bounds<D>(p.centers + c * D, lo, hi, p.infl[c], lb_, ub_);
       if (lb_ <= U) {
-        int slot = atomicAdd(&s_ncand, 1);
+        const int slot = atomicAdd(&s_ncand, 1);
         if (slot < CAP) stage_center<D>(S, slot, c, p.centers, p.infl);
       }
     }
     __syncthreads();
     const int ncand = s_ncand;
-    const bool overflow = ncand > CAP;   // then stream the whole source in chunks
+    const bool overflow = ncand > CAP;  // then stream the whole source in chunks
     const int total = overflow ? nsrc : ncand;
 
-    // ---- 4. scan (kmeans.py:326-344) with an approximate prefilter:
-    // pass 1 finds the two smallest q = d^2/infl^2; pass 2 evaluates the
-    // reference's exact effective distance only where q <= q2 (1 + Q_TOL),
-    // a superset of every center whose exact distance is <= the exact runner-up.
-    double x[PPT][D], q1[PPT], q2[PPT];
+    double q1[SPT], q2[SPT];
 #pragma unroll
-    for (int r = 0; r < PPT; ++r) {
-      int s = tid + r * AT;
-      q1[r] = INFINITY;
-      q2[r] = INFINITY;
-      if (r < ppt && s < nscan) {
-        int q = s_pos[s];
-#pragma unroll
-        for (int j = 0; j < D; ++j) x[r][j] = p.X[j * p.ldx + q];
-      }
-    }
+    for (int r = 0; r < SPT; ++r) q1[r] = q2[r] = INFINITY;
     for (int c0 = 0; c0 < total; c0 += CAP) {
       const int cn = min(CAP, total - c0);
       if (overflow) {
         __syncthreads();
-        for (int i = tid; i < cn; i += AT) {
-          int c = src ? src[c0 + i] : c0 + i;
-          stage_center<D>(S, i, c, p.centers, p.infl);
-        }
+        for (int i = tid; i < cn; i += AT)
+          stage_center<D>(S, i, src ? src[c0 + i] : c0 + i, p.centers, p.infl);
         __syncthreads();
       }
 #pragma unroll
-      for (int r = 0; r < PPT; ++r) {
-        if (r < ppt && tid + r * AT < nscan) {
+      for (int r = 0; r < SPT; ++r) {
+        if (qpos[r] >= 0) {
           double a1 = q1[r], a2 = q2[r];
           int i = 0;
           for (; i + 4 <= cn; i += 4) {
@@ -299,10 +423,10 @@ __global__ void __launch_bounds__(AT, 2) assign_kernel(gp_assign_args p, int ppt
         }
       }
     }
-    double best[PPT], second[PPT], thr[PPT];
-    int bi[PPT];
+    double best[SPT], second[SPT], thr[SPT];
+    int bi[SPT];
 #pragma unroll
-    for (int r = 0; r < PPT; ++r) {
+    for (int r = 0; r < SPT; ++r) {
       best[r] = INFINITY;
       second[r] = INFINITY;
       bi[r] = 0x7fffffff;
@@ -312,23 +436,21 @@ __global__ void __launch_bounds__(AT, 2) assign_kernel(gp_assign_args p, int ppt
       const int cn = min(CAP, total - c0);
       if (overflow) {
         __syncthreads();
-        for (int i = tid; i < cn; i += AT) {
-          int c = src ? src[c0 + i] : c0 + i;
-          stage_center<D>(S, i, c, p.centers, p.infl);
-        }
+        for (int i = tid; i < cn; i += AT)
+          stage_center<D>(S, i, src ? src[c0 + i] : c0 + i, p.centers, p.infl);
         __syncthreads();
       }
 #pragma unroll
-      for (int r = 0; r < PPT; ++r) {
-        if (r < ppt && tid + r * AT < nscan) {
+      for (int r = 0; r < SPT; ++r) {
+        if (qpos[r] >= 0) {
           for (int i = 0; i < cn; ++i) {
             if (qdist<D>(x[r], S, i) <= thr[r]) {
               double cc[D];
 #pragma unroll
               for (int j = 0; j < D; ++j) cc[j] = S.c[j][i];
-              double dist = effdist_rn<D>(x[r], cc, S.inf[i], p.order3);
-              int cid = S.cid[i];
-              bool win = dist < best[r] || (dist == best[r] && cid < bi[r]);
+              const double dist = effdist_rn<D>(x[r], cc, S.inf[i], p.order3);
+              const int cid = S.cid[i];
+              const bool win = dist < best[r] || (dist == best[r] && cid < bi[r]);
               second[r] = win ? best[r] : fmin(second[r], dist);
               best[r] = win ? dist : best[r];
               bi[r] = win ? cid : bi[r];
@@ -338,56 +460,37 @@ __global__ void __launch_bounds__(AT, 2) assign_kernel(gp_assign_args p, int ppt
         }
       }
     }
+    // ---- write back + block weights of the scanned points
 #pragma unroll
-    for (int r = 0; r < PPT; ++r) {
-      int s = tid + r * AT;
-      if (r < ppt && s < nscan) {
-        int q = s_pos[s];
-        int c = bi[r];
+    for (int r = 0; r < SPT; ++r) {
+      const bool valid = qpos[r] >= 0;
+      int c = -1;
+      long long v = 0;
+      if (valid) {
+        const int q = qpos[r];
+        c = bi[r];
         p.a[q] = c;
         p.ub[q] = __ddiv_ru(__dsub_ru(best[r], p.ub_shift[c]), p.ub_scale[c]);
         p.lb[q] = __ddiv_rd(__dadd_rd(second[r], p.lb_shift), p.lb_scale);
-        s_newa[s_ent[s]] = c;
+        v = weight_units<WM>(p.w, q, wshift);
+      }
+      const unsigned grp = __match_any_sync(FULL, c);
+      if (grp == FULL) {
+        long long g = v;
+        for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(FULL, g, o);
+        if (lane == 0 && valid) cache_add(s_ckey, s_cval, p.block_w, c, g);
+      } else if (valid) {
+        cache_add(s_ckey, s_cval, p.block_w, c, v);
       }
     }
   }
-  __syncthreads();
-
-  // ---- 5. block weights (exact int64, kmeans.py:368-374) + counters
-#pragma unroll
-  for (int e = 0; e < PPT; ++e) {
-    if (e >= ppt) break;
-    int ent = e * AT + tid;
-    int a = cur[e];
-    if (pos[e] >= 0 && ((s_scanned[ent >> 5] >> (ent & 31)) & 1u)) a = s_newa[ent];
-    bool valid = pos[e] >= 0 && a >= 0;
-    long long v = valid ? (long long)(wv[e] * p.wscale) : 0;
-    unsigned grp = __match_any_sync(FULL, valid ? a : -1);
-    if (grp == FULL) {
-      // SFC order makes whole-warp groups the common case: one smem atomic per warp
-      long long gsum = v;
-      for (int o = 16; o; o >>= 1) gsum += __shfl_xor_sync(FULL, gsum, o);
-      if (lane == 0 && valid) cache_add(s_ckey, s_cval, p.block_w, a, gsum);
-    } else if (valid) {
-      cache_add(s_ckey, s_cval, p.block_w, a, v);
-    }
-  }
-  unsigned long long c0 = nskip, c1 = ndec, c2 = nevals;
-  for (int o = 16; o; o >>= 1) {
-    c0 += __shfl_xor_sync(FULL, c0, o);
-    c1 += __shfl_xor_sync(FULL, c1, o);
-    c2 += __shfl_xor_sync(FULL, c2, o);
-  }
-  if (lane == 0) {
-    atomicAdd(&s_cnt[0], c0);
-    atomicAdd(&s_cnt[1], c1);
-    atomicAdd(&s_cnt[2], c2);
-  }
+  }  // chunk loop
+  for (int o = 16; o; o >>= 1) nevals += __shfl_xor_sync(FULL, nevals, o);
+  if (lane == 0 && nevals) atomicAdd(&p.counters[2], nevals);
   __syncthreads();
   for (int i = tid; i < HSLOTS; i += AT)
     if (s_ckey[i] >= 0 && s_cval[i] != 0)
       atomicAdd((unsigned long long*)&p.block_w[s_ckey[i]], (unsigned long long)s_cval[i]);
-  if (tid < 3 && s_cnt[tid]) atomicAdd(&p.counters[tid], s_cnt[tid]);
 }
 
 // ------------------------------------------------------------------ audit
@@ -454,21 +557,57 @@ using namespace gp;
 
 extern "C" {
 
+int gp_assign_workspace_bytes(int64_t m, size_t* bytes) {
+  GP_REQUIRE(m >= 0 && m < (1ll << 31), "gp_assign_workspace_bytes: m out of range");
+  *bytes = assign_layout(m).total;
+  return GP_OK;
+}
+
 int gp_assign_round(const gp_assign_args* args, void* stream) {
   int rc = validate(args);
   if (rc) return rc;
   if (args->m == 0) return GP_OK;
-  // tile size: 4 entries per thread when the grid is big enough, fewer for the
-  // small sample-phase lists so that they still spread over the SMs
-  int ppt = args->m >= (int64_t)AT * 4 * 296 ? 4 : (args->m >= (int64_t)AT * 2 * 296 ? 2 : 1);
-  if (args->group_list) {
-    GP_REQUIRE((int64_t)AT * ppt <= (1ll << args->group_shift),
-               "group_shift smaller than the tile");
-  }
-  unsigned grid = grid_for(args->m, AT * ppt);
+  AssignLayout L = assign_layout(args->m);
+  GP_REQUIRE(args->workspace && args->workspace_bytes >= L.total,
+             "gp_assign_round: workspace too small");
+  if (args->group_list)
+    GP_REQUIRE(FCHUNK <= (1ll << args->group_shift), "group_shift smaller than a filter chunk");
   cudaStream_t s = (cudaStream_t)stream;
-  if (args->d == 2) assign_kernel<2><<<grid, AT, 0, s>>>(*args, ppt);
-  else assign_kernel<3><<<grid, AT, 0, s>>>(*args, ppt);
+  char* ws = (char*)args->workspace;
+  int32_t* scan = (int32_t*)(ws + L.off_list);
+  int32_t* runs = (int32_t*)(ws + L.off_runs);
+  // exact weight units: wscale = 2^wshift
+  int wshift = 0;
+  frexp(args->wscale, &wshift);
+  wshift -= 1;
+  GP_REQUIRE(ldexp(1.0, wshift) == args->wscale, "gp_assign_round: wscale must be a power of 2");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nc = L.nchunks;
+  // persistent grids: exactly the co-resident CTAs (static chunk split in the filter)
+  auto fit = [&](const void* fn, int threads) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+    int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    return (unsigned)(nc < g ? nc : g);
+  };
+#define GP_LAUNCH_ASSIGN(WM)                                                                     \
+  {                                                                                              \
+    unsigned gf = fit((const void*)filter_kernel<WM>, FTH);                                      \
+    filter_kernel<WM><<<gf, FTH, 0, s>>>(*args, wshift, nc, scan, runs);                         \
+    if (args->d == 2) {                                                                          \
+      unsigned gs = fit((const void*)scan_kernel<2, WM>, AT);                                    \
+      scan_kernel<2, WM><<<gs, AT, 0, s>>>(*args, wshift, nc, scan, runs);                       \
+    } else {                                                                                     \
+      unsigned gs = fit((const void*)scan_kernel<3, WM>, AT);                                    \
+      scan_kernel<3, WM><<<gs, AT, 0, s>>>(*args, wshift, nc, scan, runs);                       \
+    }                                                                                            \
+  }
+  if (args->wmode == GP_W_UNIT) { GP_LAUNCH_ASSIGN(GP_W_UNIT) }
+  else if (args->wmode == GP_W_F32) { GP_LAUNCH_ASSIGN(GP_W_F32) }
+  else { GP_LAUNCH_ASSIGN(GP_W_F64) }
+#undef GP_LAUNCH_ASSIGN
   return check_launch("assign_round");
 }
 

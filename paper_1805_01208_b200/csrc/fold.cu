@@ -4,35 +4,36 @@
 // folds in SFC order (ranksim.py:173-197), then folds the 256 segment partials
 // sequentially (np.add.reduce(axis=0), ranksim.py:218-222 / kmeans.py:374).
 // A sequential fold cannot be parallelised, but the folds of different
-// (segment, block) pairs are independent, and SFC order keeps each block in a
-// short span of positions.  So:
-//   discover : per (segment, block) the first/last local position (warp
-//              aggregated atomics on a dense S x k table);
-//   pairs    : compact the non-empty (segment, block) cells into a work list;
-//   fold     : one warp per pair walks its span in 32-wide chunks, stages the
-//              chunk's values in shared memory and lets lane j fold column j
-//              in position order (the exact bincount order); extents (max
+// (segment, block) pairs are independent.  SFC order keeps a block in a few
+// runs of consecutive positions, so:
+//   runs     : every maximal run of positions with the same (segment, block)
+//              key (stable compaction of the key-change positions);
+//   group    : stable radix sort of the runs by key -> each pair's runs in
+//              position order; pair boundaries -> work list;
+//   fold     : one warp per pair walks its runs in order, stages each chunk's
+//              values in shared memory and lets lane j fold column j in
+//              position order (the exact bincount order); extents (max
 //              distance to the old center, kmeans.py:474-487) and the
 //              objective terms (kmeans.py:490-499) are computed in parallel
 //              by all lanes of the chunk;
 //   combine  : per block, fold the pair partials in segment order.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
 #include "common.cuh"
 
 namespace gp {
 
-struct Pair {
-  int32_t key;  // local_segment * k + block
-  int32_t first;
-  int32_t last;
-  int32_t pad;
-};
+constexpr int FT = 256;     // threads per fold CTA (8 warps)
+constexpr int MAXCOL = 5;   // d wx columns + w + objective (d <= 3)
+constexpr int FB = 4;       // chunks of 32 positions prefetched per batch
 
-constexpr int FT = 256;           // threads per fold CTA (8 warps)
-constexpr int MAXCOL = 5;         // d wx columns + w + objective (d <= 3)
-
+// counters[]: 0 runs, 1 work cursor, 2 valid runs, 3 pairs
 struct FoldLayout {
-  int64_t s0, nseg, cells, max_pairs;
-  size_t off_first, off_last, off_slot, off_pairs, off_out, off_counters, total;
+  int64_t s0, nseg, cells, cap, pcap;
+  size_t off_flags, off_starts, off_rkey, off_skey, off_sidx, off_ridx, off_pbeg, off_slot,
+      off_out, off_counters, off_cub, cub_bytes, total;
 };
 
 static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k) {
@@ -42,84 +43,107 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   int64_t s1 = n_local > 0 ? seg(pos0 + n_local - 1) : 0;
   L.nseg = n_local > 0 ? s1 - L.s0 + 1 : 1;
   L.cells = L.nseg * k;
-  L.max_pairs = L.cells < n_local ? L.cells : (n_local > 0 ? n_local : 1);
+  L.cap = n_local > 0 ? n_local : 1;
+  L.pcap = L.cells < L.cap ? L.cells : L.cap;  // pairs <= min(segments x blocks, runs)
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceSelect::Flagged(nullptr, b1, cub::CountingInputIterator<int32_t>(0),
+                             (const uint8_t*)nullptr, (int32_t*)nullptr, (int64_t*)nullptr,
+                             (int)L.cap);
+  cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, b2, kb, vb, (int)L.cap, 0, 32);
+  L.cub_bytes = b1 > b2 ? b1 : b2;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   size_t o = 0;
-  L.off_first = o; o = al(o + L.cells * sizeof(int32_t));
-  L.off_last = o; o = al(o + L.cells * sizeof(int32_t));
-  L.off_slot = o; o = al(o + L.cells * sizeof(int32_t));
-  L.off_pairs = o; o = al(o + L.max_pairs * sizeof(Pair));
-  L.off_out = o; o = al(o + L.max_pairs * (MAXCOL + 1) * sizeof(double));
-  L.off_counters = o; o = al(o + 4 * sizeof(int64_t));
+  L.off_flags = o; o = al(o + L.cap);
+  L.off_starts = o; o = al(o + (L.cap + 1) * 4);
+  L.off_rkey = o; o = al(o + L.cap * 4);
+  L.off_skey = o; o = al(o + L.cap * 4);
+  L.off_sidx = o; o = al(o + L.cap * 4);
+  L.off_ridx = o; o = al(o + L.cap * 4);
+  L.off_pbeg = o; o = al(o + (L.pcap + 1) * 4);
+  L.off_slot = o; o = al(o + L.cells * 4);
+  L.off_out = o; o = al(o + L.pcap * (MAXCOL + 1) * sizeof(double));
+  L.off_counters = o; o = al(o + 8 * sizeof(int64_t));
+  L.off_cub = o; o = al(o + L.cub_bytes);
   L.total = o;
   return L;
 }
 
-__global__ void fold_init(int32_t* first, int32_t* last, int64_t cells, int64_t* counters) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cells;
+__device__ __forceinline__ int32_t fold_key(const int32_t* a, int64_t i, int64_t pos0,
+                                            int64_t n_global, int64_t s0, int k) {
+  int c = a[i];
+  return c >= 0 ? (int32_t)((segment_of(pos0 + i, n_global) - s0) * k + c) : -1;
+}
+
+// flag every position whose key differs from its predecessor's (run starts)
+__global__ void fold_mark(const int32_t* __restrict__ a, int64_t n_local, int64_t pos0,
+                          int64_t n_global, int64_t s0, int k, uint8_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_local;
        i += (int64_t)gridDim.x * blockDim.x) {
-    first[i] = 0x7fffffff;
-    last[i] = -1;
-  }
-  if (blockIdx.x == 0 && threadIdx.x < 4) counters[threadIdx.x] = 0;
-}
-
-__global__ void fold_discover(const int32_t* __restrict__ a, int64_t n_local, int64_t pos0,
-                              int64_t n_global, int64_t s0, int k, int32_t* first,
-                              int32_t* last) {
-  int lane = threadIdx.x & 31;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n_local; base += stride) {
-    int64_t i = base + threadIdx.x;
-    int key = -1;
-    if (i < n_local) {
-      int c = a[i];
-      if (c >= 0) key = (int)((segment_of(pos0 + i, n_global) - s0) * k + c);
-    }
-    unsigned grp = __match_any_sync(FULL, key);
-    if (key >= 0 && lane == __ffs(grp) - 1) {
-      int hi_lane = 31 - __clz(grp);
-      atomicMin(&first[key], (int32_t)i);
-      atomicMax(&last[key], (int32_t)(i - lane + hi_lane));
-    }
+    int32_t key = fold_key(a, i, pos0, n_global, s0, k);
+    int32_t prev = i > 0 ? fold_key(a, i - 1, pos0, n_global, s0, k) : -2;
+    flags[i] = key != prev;
   }
 }
 
-__global__ void fold_pairs(const int32_t* __restrict__ first, const int32_t* __restrict__ last,
-                           int64_t cells, int32_t* slot, Pair* pairs, int64_t* counters) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cells;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t l = last[i];
-    if (l >= 0) {
-      int64_t p = atomicAdd((unsigned long long*)&counters[0], 1ull);
-      pairs[p] = Pair{(int32_t)i, first[i], l, 0};
-      slot[i] = (int32_t)p;
-    } else {
-      slot[i] = -1;
-    }
+// run r -> (key, r); runs with key -1 (unassigned / inactive) sort last
+__global__ void fold_run_keys(const int32_t* __restrict__ a, int32_t* __restrict__ starts,
+                              int64_t R, int64_t* counters, int64_t n_local, int64_t pos0,
+                              int64_t n_global, int64_t s0, int k, uint32_t* __restrict__ rkey,
+                              int32_t* __restrict__ ridx) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) starts[R] = (int32_t)n_local;  // sentinel end
+  int valid = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int32_t key = fold_key(a, starts[r], pos0, n_global, s0, k);
+    rkey[r] = (uint32_t)key;  // -1 -> 0xffffffff
+    ridx[r] = (int32_t)r;
+    valid += key >= 0;
   }
+  for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(FULL, valid, o);
+  if ((threadIdx.x & 31) == 0 && valid)
+    atomicAdd((unsigned long long*)&counters[2], (unsigned long long)valid);
 }
 
-// One warp per (segment, block) pair.  The span [first, last] is walked in
-// batches of FB chunks of 32 positions: every load of a batch is issued before
-// any of its values is consumed (one memory latency per batch instead of one
-// per chunk), then lane j folds column j over the matched positions in order.
-constexpr int FB = 4;
+// first sorted run of every pair (valid runs occupy the first counters[2] slots)
+__global__ void fold_pair_flags(const uint32_t* __restrict__ skey, int64_t R,
+                                const int64_t* counters, uint8_t* __restrict__ flags) {
+  const int64_t V = counters[2];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < R;
+       j += (int64_t)gridDim.x * blockDim.x)
+    flags[j] = j < V && (j == 0 || skey[j] != skey[j - 1]);
+}
 
+__global__ void fold_slots(const uint32_t* __restrict__ skey, int32_t* __restrict__ pbeg,
+                           const int64_t* counters, int32_t* __restrict__ slot) {
+  const int64_t P = counters[3];
+  if (blockIdx.x == 0 && threadIdx.x == 0) pbeg[P] = (int32_t)counters[2];  // sentinel end
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x)
+    slot[skey[pbeg[p]]] = (int32_t)p;
+}
+
+// One warp per (segment, block) pair: its runs in position order, each run in
+// batches of FB chunks of 32 positions whose loads are all issued before any
+// value is consumed; lane j then folds column j over the batch in order.
 template <int D>
-__global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const Pair* __restrict__ pairs,
-                                                  int64_t* counters, double* out) {
+__global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const int32_t* __restrict__ starts,
+                                                  const uint32_t* __restrict__ skey,
+                                                  const int32_t* __restrict__ sidx,
+                                                  const int32_t* __restrict__ pbeg,
+                                                  int64_t* counters, double* __restrict__ out) {
   __shared__ double sm[FT / 32][MAXCOL][FB * 32 + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ncols = f.weights_only ? 1 : D + 2;
-  const int64_t npairs = counters[0];
+  const int64_t npairs = counters[3];
   for (;;) {
     int64_t pi;
     if (lane == 0) pi = (int64_t)atomicAdd((unsigned long long*)&counters[1], 1ull);
     pi = __shfl_sync(FULL, pi, 0);
     if (pi >= npairs) break;
-    const Pair pr = pairs[pi];
-    const int c = pr.key % f.k;
+    const int j0 = pbeg[pi], j1 = pbeg[pi + 1];
+    const int c = (int)(skey[j0] % (uint32_t)f.k);
     double cold[D];
     if (!f.weights_only) {
 #pragma unroll
@@ -127,60 +151,53 @@ __global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const Pair* __
     }
     double acc = 0.0;  // lane j < ncols folds column j; bincount starts from 0.0
     double ext = 0.0;
-    for (int64_t base = pr.first; base <= pr.last; base += FB * 32) {
-      int av[FB];
-      double xv[FB][D], wv[FB];
-#pragma unroll
-      for (int b = 0; b < FB; ++b) {
-        int64_t i = base + b * 32 + lane;
-        bool in = i <= pr.last;
-        av[b] = in ? f.a[i] : -1;
-        wv[b] = in ? load_weight(f.w, f.wmode, i) : 0.0;
-        if (!f.weights_only) {
-#pragma unroll
-          for (int j = 0; j < D; ++j) xv[b][j] = in ? f.X[j * f.ldx + i] : 0.0;
-        }
-      }
-      unsigned masks[FB];
-#pragma unroll
-      for (int b = 0; b < FB; ++b) {
-        bool valid = av[b] == c;
-        masks[b] = __ballot_sync(FULL, valid);
-        const int slot = b * 32 + lane;
-        if (f.weights_only) {
-          sm[warp][0][slot] = wv[b];
-        } else {
-          double diff[D];
-#pragma unroll
-          for (int j = 0; j < D; ++j) {
-            sm[warp][j][slot] = __dmul_rn(xv[b][j], wv[b]);  // wx = points * weights[:, None]
-            diff[j] = __dsub_rn(xv[b][j], cold[j]);
-          }
-          double sq = sqnorm_rn(diff, D, f.order3);
-          sm[warp][D][slot] = wv[b];
-          sm[warp][D + 1][slot] = __dmul_rn(sq, wv[b]);
-          if (valid) ext = fmax(ext, __dsqrt_rn(sq));
-        }
-      }
-      __syncwarp();
-      if (lane < ncols) {
-        const double* col = sm[warp][lane];
+    for (int jr = j0; jr < j1; ++jr) {
+      const int r = sidx[jr];
+      const int64_t rb = starts[r], re = starts[r + 1];  // every position in [rb, re) is block c
+      for (int64_t base = rb; base < re; base += FB * 32) {
+        double xv[FB][D], wv[FB];
 #pragma unroll
         for (int b = 0; b < FB; ++b) {
-          unsigned m = masks[b];
-          if (m == FULL) {
+          int64_t i = base + b * 32 + lane;
+          bool in = i < re;
+          wv[b] = in ? load_weight(f.w, f.wmode, i) : 0.0;
+          if (!f.weights_only) {
 #pragma unroll
-            for (int t = 0; t < 32; ++t) acc = __dadd_rn(acc, col[b * 32 + t]);
-          } else {
-            while (m) {
-              int t = __ffs(m) - 1;
-              m &= m - 1;
-              acc = __dadd_rn(acc, col[b * 32 + t]);
-            }
+            for (int j = 0; j < D; ++j) xv[b][j] = in ? f.X[j * f.ldx + i] : 0.0;
           }
         }
+#pragma unroll
+        for (int b = 0; b < FB; ++b) {
+          const int slot = b * 32 + lane;
+          const bool in = base + slot < re;
+          if (f.weights_only) {
+            sm[warp][0][slot] = wv[b];
+          } else {
+            double diff[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              sm[warp][j][slot] = __dmul_rn(xv[b][j], wv[b]);  // wx = points * weights[:, None]
+              diff[j] = __dsub_rn(xv[b][j], cold[j]);
+            }
+            double sq = sqnorm_rn(diff, D, f.order3);
+            sm[warp][D][slot] = wv[b];
+            sm[warp][D + 1][slot] = __dmul_rn(sq, wv[b]);
+            if (in) ext = fmax(ext, __dsqrt_rn(sq));
+          }
+        }
+        __syncwarp();
+        const int cnt = (int)min((int64_t)(FB * 32), re - base);
+        if (lane < ncols) {
+          const double* col = sm[warp][lane];
+          if (cnt == FB * 32) {
+#pragma unroll 32
+            for (int t = 0; t < FB * 32; ++t) acc = __dadd_rn(acc, col[t]);
+          } else {
+            for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, col[t]);
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
     for (int o = 16; o; o >>= 1) ext = fmax(ext, __shfl_xor_sync(FULL, ext, o));
     double* po = out + pi * (MAXCOL + 1);
@@ -195,13 +212,9 @@ template <int D>
 __global__ void fold_combine(gp_fold_args f, const int32_t* __restrict__ slot, int64_t nseg,
                              const double* __restrict__ out) {
   __shared__ int32_t s_slot[4][GP_SEGMENTS];
-  __shared__ int s_cnt[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 4 + warp;
   if (c >= f.k) return;
-  // ordered compaction of the present segments
-  if (lane == 0) s_cnt[warp] = 0;
-  __syncwarp();
   int base = 0;
   for (int64_t s0 = 0; s0 < nseg; s0 += 32) {
     int64_t s = s0 + lane;
@@ -215,20 +228,17 @@ __global__ void fold_combine(gp_fold_args f, const int32_t* __restrict__ slot, i
   const int ncols = f.weights_only ? 1 : D + 2;
   if (lane < ncols) {
     double acc = 0.0;
-    for (int i = 0; i < np; ++i) acc = __dadd_rn(acc, out[(int64_t)s_slot[warp][i] * (MAXCOL + 1) + lane]);
-    if (f.weights_only) {
-      f.wsum[c] = acc;
-    } else if (lane < D) {
-      f.sums[c * D + lane] = acc;
-    } else if (lane == D) {
-      f.wsum[c] = acc;
-    } else {
-      f.objective[c] = acc;
-    }
+    for (int i = 0; i < np; ++i)
+      acc = __dadd_rn(acc, out[(int64_t)s_slot[warp][i] * (MAXCOL + 1) + lane]);
+    if (f.weights_only) f.wsum[c] = acc;
+    else if (lane < D) f.sums[c * D + lane] = acc;
+    else if (lane == D) f.wsum[c] = acc;
+    else f.objective[c] = acc;
   }
   if (!f.weights_only) {
     double ext = 0.0;
-    for (int i = lane; i < np; i += 32) ext = fmax(ext, out[(int64_t)s_slot[warp][i] * (MAXCOL + 1) + MAXCOL]);
+    for (int i = lane; i < np; i += 32)
+      ext = fmax(ext, out[(int64_t)s_slot[warp][i] * (MAXCOL + 1) + MAXCOL]);
     for (int o = 16; o; o >>= 1) ext = fmax(ext, __shfl_xor_sync(FULL, ext, o));
     if (lane == 0) f.extent[c] = ext;
   }
@@ -260,27 +270,53 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
   GP_REQUIRE(L.cells < (1ll << 31), "gp_movement_fold: segment x block table too large");
   cudaStream_t s = (cudaStream_t)stream;
   char* ws = (char*)f->workspace;
-  int32_t* first = (int32_t*)(ws + L.off_first);
-  int32_t* last = (int32_t*)(ws + L.off_last);
+  uint8_t* flags = (uint8_t*)(ws + L.off_flags);
+  int32_t* starts = (int32_t*)(ws + L.off_starts);
+  uint32_t* rkey = (uint32_t*)(ws + L.off_rkey);
+  uint32_t* skey = (uint32_t*)(ws + L.off_skey);
+  int32_t* sidx = (int32_t*)(ws + L.off_sidx);
+  int32_t* ridx = (int32_t*)(ws + L.off_ridx);
+  int32_t* pbeg = (int32_t*)(ws + L.off_pbeg);
   int32_t* slot = (int32_t*)(ws + L.off_slot);
-  Pair* pairs = (Pair*)(ws + L.off_pairs);
   double* out = (double*)(ws + L.off_out);
   int64_t* counters = (int64_t*)(ws + L.off_counters);
+  void* cub_tmp = ws + L.off_cub;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n = f->n_local;
 
-  fold_init<<<grid_for(L.cells, 256, sms * 8), 256, 0, s>>>(first, last, L.cells, counters);
-  if (f->n_local > 0)
-    fold_discover<<<grid_for(f->n_local, 256, sms * 16), 256, 0, s>>>(
-        f->a, f->n_local, f->pos0, f->n_global, L.s0, f->k, first, last);
-  fold_pairs<<<grid_for(L.cells, 256, sms * 8), 256, 0, s>>>(first, last, L.cells, slot, pairs,
-                                                             counters);
+  GP_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(int64_t), s));
+  GP_CUDA(cudaMemsetAsync(slot, 0xff, L.cells * sizeof(int32_t), s));
+  if (n > 0) {
+    fold_mark<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(f->a, n, f->pos0, f->n_global, L.s0,
+                                                          f->k, flags);
+    size_t b = L.cub_bytes;
+    GP_CUDA(cub::DeviceSelect::Flagged(cub_tmp, b, cub::CountingInputIterator<int32_t>(0), flags,
+                                       starts, counters + 0, (int)n, s));
+    int64_t R = 0;
+    GP_CUDA(cudaMemcpyAsync(&R, counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    GP_CUDA(cudaStreamSynchronize(s));
+    fold_run_keys<<<grid_for(R, 256, sms * 16), 256, 0, s>>>(
+        f->a, starts, R, counters, n, f->pos0, f->n_global, L.s0, f->k, rkey, ridx);
+    // stable LSD radix sort with ping-pong buffers (no n-sized CUB scratch)
+    cub::DoubleBuffer<uint32_t> kb(rkey, skey);
+    cub::DoubleBuffer<int32_t> vb(ridx, sidx);
+    b = L.cub_bytes;
+    GP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, b, kb, vb, (int)R, 0, 32, s));
+    skey = kb.Current();
+    sidx = vb.Current();
+    fold_pair_flags<<<grid_for(R, 256, sms * 16), 256, 0, s>>>(skey, R, counters, flags);
+    b = L.cub_bytes;
+    GP_CUDA(cub::DeviceSelect::Flagged(cub_tmp, b, cub::CountingInputIterator<int32_t>(0), flags,
+                                       pbeg, counters + 3, (int)R, s));
+    fold_slots<<<grid_for(R, 256, sms * 8), 256, 0, s>>>(skey, pbeg, counters, slot);
+  }
   if (f->d == 2) {
-    fold_kernel<2><<<sms * 8, FT, 0, s>>>(*f, pairs, counters, out);
+    fold_kernel<2><<<sms * 6, FT, 0, s>>>(*f, starts, skey, sidx, pbeg, counters, out);
     fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   } else {
-    fold_kernel<3><<<sms * 8, FT, 0, s>>>(*f, pairs, counters, out);
+    fold_kernel<3><<<sms * 6, FT, 0, s>>>(*f, starts, skey, sidx, pbeg, counters, out);
     fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   }
   return check_launch("movement_fold");

@@ -28,6 +28,8 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -110,6 +112,29 @@ class _Timer:
         return sum(a.elapsed_time(b) for a, b in self.events)
 
 
+def sample_ranks_device(n: int, seed: int, device, stream) -> torch.Tensor:
+    """Inverse of numpy.random.default_rng(seed).permutation(n), computed on the GPU.
+
+    Bit-exact with numpy (gp_sample_ranks reproduces PCG64 + the masked
+    rejection draws + the descending Fisher-Yates swaps); set
+    GP_HOST_PERMUTATION=1 to compute it with host numpy instead (verification).
+    """
+    if os.environ.get("GP_HOST_PERMUTATION") == "1":
+        perm = np.random.default_rng(seed).permutation(n)
+        rank = np.empty(n, dtype=np.int32)
+        rank[perm] = np.arange(n, dtype=np.int32)
+        return torch.from_numpy(rank).to(device)
+    st = np.random.PCG64(seed).state["state"]
+    m64 = (1 << 64) - 1
+    words = (C.c_uint64 * 4)(st["state"] >> 64, st["state"] & m64, st["inc"] >> 64,
+                             st["inc"] & m64)
+    rank = torch.empty(n, dtype=torch.int32, device=device)
+    wsb = N.size_query("gp_sample_ranks_workspace_bytes", n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+    N.call("gp_sample_ranks", words, n, rank.data_ptr(), ws.data_ptr(), wsb, stream)
+    return rank
+
+
 class _Hierarchy:
     """Group-level candidate lists (gp_group_boxes / gp_group_candidates).
 
@@ -122,7 +147,7 @@ class _Hierarchy:
     SUPER_CAP, MEGA_CAP = 1024, 4096
 
     def __init__(self, eng, use_mega: bool):
-        self.eng = eng
+        self.eng = weakref.proxy(eng)  # no engine <-> hierarchy cycle keeping GBs alive
         self.use_mega = use_mega
         self.key = None
 
@@ -169,8 +194,10 @@ class _Hierarchy:
 class DevicePartitioner:
     """One partition run on one GPU (the whole point set is one SFC shard)."""
 
-    def __init__(self, settings: KMeansSettings, device=None, timer: _Timer | None = None):
+    def __init__(self, settings: KMeansSettings, device=None, timer: _Timer | None = None,
+                 keep_keys: bool = False):
         self.settings = settings
+        self.keep_keys = keep_keys
         self.device = torch.device(device if device is not None else "cuda")
         self.timer = timer
         self.order3 = einsum_order3()
@@ -246,8 +273,8 @@ class DevicePartitioner:
         ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
         N.call("gp_sort_pairs", keys.data_ptr(), gids.data_ptr(), keys_s.data_ptr(),
                self.gids.data_ptr(), n, d * depth, ws.data_ptr(), wsb, sh)
-        self.keys_sorted = keys_s
-        del keys, gids, ws
+        self.keys_sorted = keys_s if self.keep_keys else None
+        del keys, gids, ws, keys_s
         self.ldx = n
         self.X = torch.empty((d, n), dtype=torch.float64, device=dev)
         self.W = None
@@ -267,10 +294,7 @@ class DevicePartitioner:
         # sample ranks in SFC order (kmeans.py:564-568)
         self.sizes = sample_schedule(n, st.init_sample)
         if self.sizes:
-            perm = np.random.default_rng(st.seed).permutation(n)
-            rank = np.empty(n, dtype=np.int32)
-            rank[perm] = np.arange(n, dtype=np.int32)
-            rank_d = torch.from_numpy(rank).to(dev)
+            rank_d = sample_ranks_device(n, st.seed, dev, sh)
             self.rank_sfc = torch.empty(n, dtype=torch.int32, device=dev)
             N.call("gp_gather_ranks", rank_d.data_ptr(), self.gids.data_ptr(), n,
                    self.rank_sfc.data_ptr(), sh)
@@ -278,6 +302,12 @@ class DevicePartitioner:
             self.compact_ws = torch.empty(max(cwb, 8), dtype=torch.uint8, device=dev)
             self.active_idx = torch.empty(n, dtype=torch.int32, device=dev)
             self.active_cnt = torch.empty(1, dtype=torch.int64, device=dev)
+            del rank_d
+        del pts, w
+        if n >= (1 << 26):
+            # hand the bootstrap's transient buffers (sort, permutation) back so the
+            # main loop's workspaces do not fragment around them
+            torch.cuda.empty_cache()
         return self
 
     # ------------------------------------------------------------ helpers
@@ -303,6 +333,9 @@ class DevicePartitioner:
         a.infl, a.ub_scale, a.ub_shift = base, base + 8 * k, base + 16 * k
         a.block_w = self.red.data_ptr()
         a.counters = self.red.data_ptr() + 8 * k
+        awb = N.size_query("gp_assign_workspace_bytes", n)
+        self.assign_ws = torch.empty(awb, dtype=torch.uint8, device=dev)
+        a.workspace, a.workspace_bytes = self.assign_ws.data_ptr(), awb
         self.aargs = a
         self.hier = _Hierarchy(self, use_mega=k > 4096) if k > 128 else None
         f = N.FoldArgs()
@@ -355,7 +388,8 @@ class DevicePartitioner:
             self.timer.events.append((e0, self.timer.mark(self.stream)))
         host = self.red.cpu().numpy()
         k = self.settings.k
-        cnt = host[k:k + 3]
+        cnt = host[k:k + 3].copy()
+        cnt[1] = self.aargs.m  # every active entry is one decision (kmeans.py:309)
         if self.timer is not None:
             self.timer.rounds.append((int(cnt[1]), int(cnt[1] - cnt[0]), int(cnt[2])))
         return host[:k], cnt
@@ -495,7 +529,15 @@ class DevicePartitioner:
             stats.skip_check_failures = int(aud[2])
         out = torch.empty(n, dtype=torch.int64, device=self.device)
         N.call("gp_scatter_by_gid", A.data_ptr(), self.gids.data_ptr(), n, out.data_ptr(), self.sh)
+        self.release()
         return out, stats
+
+    def release(self):
+        """Drop every n-sized device buffer (the caller keeps only the result)."""
+        for name in ("X", "W", "A", "A_fb", "UB", "LB", "gids", "rank_sfc", "active_idx",
+                     "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier"):
+            if hasattr(self, name):
+                setattr(self, name, None)
 
 
 def partition_device(points, weights, settings: KMeansSettings, device=None, timer=None):

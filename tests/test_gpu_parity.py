@@ -79,7 +79,7 @@ def test_sfc_stage_bit_exact_vs_reference_golden(name):
     spec = next(s for s in cases.SFC_CASES if s["name"] == name)
     gold = golden_io.load("sfc_" + name)
     pts, w = cases.partition_inputs(spec)
-    eng = DevicePartitioner(KMeansSettings(k=spec["settings"]["k"]))
+    eng = DevicePartitioner(KMeansSettings(k=spec["settings"]["k"]), keep_keys=True)
     eng.bootstrap(pts, w)
     gids = eng.gids.cpu().numpy().astype(np.int64)
     keys_sorted = eng.keys_sorted.cpu().numpy().view(np.uint64)
