@@ -16,7 +16,8 @@
  *  - Not re-entrant on the same buffers.
  *  - Coordinates are float64.  Inputs in the caller's layout are described by
  *    (stride_pt, stride_dim) in elements: AoS (n,d) row-major is (d, 1), SoA
- *    (d,n) is (1, ld).  The library's own working layout is SoA (d rows of ld).
+ *    (d,n) is (1, ld).  The library's own working layout is AoS in SFC order:
+ *    point i at X[i*ldx .. i*ldx+d) with ldx = d (one 16-byte load per 2D point).
  */
 #ifndef GEOPART_B200_H
 #define GEOPART_B200_H
@@ -77,13 +78,13 @@ int gp_sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* ke
                   size_t workspace_bytes, void* stream);
 
 /* Payload gather after the sort: replaces the fancy-indexing redistribution of
- * ranksim.py:159-168.  X (SoA, rows of ldx) <- pts[gids]; w_out (float or
+ * ranksim.py:159-168.  X (AoS, point stride ldx) <- pts[gids]; w_out (float or
  * double per wmode; ignored for GP_W_UNIT) <- w_in[gids]. */
 int gp_gather_points(const double* pts, int64_t stride_pt, int64_t stride_dim, int d,
                      const uint32_t* gids, int64_t n, double* X, int64_t ldx,
                      const double* w_in, int wmode, void* w_out, void* stream);
 
-/* K4  initial centers: rows[i] = X[:, positions[i]] (kmeans.py:552-558). */
+/* K4  initial centers: rows[i] = X[positions[i], :] (kmeans.py:552-558). */
 int gp_gather_rows(const double* X, int64_t ldx, int d, const int64_t* positions, int k,
                    double* rows, void* stream);
 
@@ -111,7 +112,7 @@ int gp_sample_ranks(const uint64_t* pcg_state, int64_t n, int32_t* rank, void* w
  * The result per point is the lowest-index argmin of the reference's
  * effective distance, bit for bit. */
 typedef struct gp_assign_args {
-  const double* X;        /* SoA coordinates, d rows of ldx */
+  const double* X;        /* AoS coordinates in SFC order, point stride ldx */
   int64_t ldx;
   int32_t d;
   int32_t k;
@@ -122,18 +123,26 @@ typedef struct gp_assign_args {
   const int32_t* list;    /* active positions (NULL: all positions 0..m-1) */
   int64_t m;              /* number of active entries */
   int32_t* a;             /* assignment per position (-1 = unassigned) */
-  double* ub;             /* normalised upper bound per position */
-  double* lb;             /* normalised lower bound per position */
+  float* ublb;            /* per position (ub~, lb~): normalised bounds, float32 rounded
+                             outward (ub~ up, lb~ down) */
   const double* centers;  /* k x d row-major */
   const double* infl;     /* k influences */
-  const double* ub_scale; /* k: ub = ub_scale[a] * ub~ + ub_shift[a] */
-  const double* ub_shift; /* k */
-  double lb_scale;        /* lb = max(lb_scale * lb~ - lb_shift, 0) */
-  double lb_shift;
+  const double* inv2_lo;  /* k: lower bound of 1/infl^2 (outward-rounded on the host) */
+  const double* inv2_hi;  /* k: upper bound of 1/infl^2 */
+  /* Lazily relaxed Hamerly bounds, float32, rounded outward:
+   *   ub = fmaf_ru(ub~ >= 0 ? E.x : E.y, ub~, E.z)      E = ub_eval[4a .. 4a+3]
+   *   lb = max(fmaf_rd(lb_a, lb~, -lb_b), 0)
+   * and after a scan with best/second effective distances b, s:
+   *   ub~ = (b - N.z) * (b - N.z >= 0 ? N.x : N.y)  rounded up, N = ub_norm[4c ..]
+   *   lb~ = (s + lb_blo) * lb_inva                 rounded down. */
+  const float* ub_eval;   /* k x 4 */
+  const float* ub_norm;   /* k x 4 */
+  float lb_a;
+  float lb_b;
+  float lb_inva;
+  float lb_blo;
   long long* block_w;     /* out: k exact block weights (units of 1/wscale), accumulated */
   unsigned long long* counters; /* out: [skips, decisions, evals], accumulated */
-  double bound_err;       /* relative error bound of the host-composed maps: evaluated
-                             bounds are widened by bound_err * (|scale*b~| + |shift|) */
   /* optional hierarchical candidate source (gp_group_candidates): entry li of
    * the active list belongs to group li >> group_shift, whose candidate centers
    * are group_list[g*group_cap .. +group_count[g]); group_count[g] < 0 means
@@ -164,9 +173,10 @@ int gp_assign_round(const gp_assign_args* args, void* stream);
 int gp_group_boxes(const double* X, int64_t ldx, int d, const int32_t* list, int64_t m,
                    int shift, double* boxes, void* stream);
 int gp_group_candidates(const double* boxes, int64_t ngroups, int d, int k,
-                        const double* centers, const double* infl, const int32_t* parent_list,
-                        const int32_t* parent_count, int parent_cap, int parent_ratio_log2,
-                        int32_t* list, int32_t* count, int cap, void* stream);
+                        const double* centers, const double* inv2_lo, const double* inv2_hi,
+                        const int32_t* parent_list, const int32_t* parent_count, int parent_cap,
+                        int parent_ratio_log2, int32_t* list, int32_t* count, int cap,
+                        void* stream);
 
 /* Re-express every bound under identity maps (when the host's cumulative
  * maps drift out of range).  Same bound semantics as gp_assign_args. */

@@ -27,9 +27,10 @@ i32, i64, u32, u64, f64, vp, sz = (C.c_int32, C.c_int64, C.c_uint32, C.c_uint64,
 class AssignArgs(C.Structure):
     _fields_ = [
         ("X", vp), ("ldx", i64), ("d", i32), ("k", i32), ("order3", i32), ("wmode", i32),
-        ("w", vp), ("wscale", f64), ("list", vp), ("m", i64), ("a", vp), ("ub", vp), ("lb", vp),
-        ("centers", vp), ("infl", vp), ("ub_scale", vp), ("ub_shift", vp), ("lb_scale", f64),
-        ("lb_shift", f64), ("block_w", vp), ("counters", vp), ("bound_err", f64),
+        ("w", vp), ("wscale", f64), ("list", vp), ("m", i64), ("a", vp), ("ublb", vp),
+        ("centers", vp), ("infl", vp), ("inv2_lo", vp), ("inv2_hi", vp), ("ub_eval", vp),
+        ("ub_norm", vp), ("lb_a", C.c_float), ("lb_b", C.c_float), ("lb_inva", C.c_float),
+        ("lb_blo", C.c_float), ("block_w", vp), ("counters", vp),
         ("group_list", vp), ("group_count", vp), ("group_cap", i32), ("group_shift", i32),
         ("workspace", vp), ("workspace_bytes", sz),
     ]
@@ -65,7 +66,7 @@ _SIGS = {
     "gp_assign_round": (C.c_int, [C.POINTER(AssignArgs), vp]),
     "gp_rebase_bounds": (C.c_int, [C.POINTER(AssignArgs), vp]),
     "gp_group_boxes": (C.c_int, [vp, i64, C.c_int, vp, i64, C.c_int, vp, vp]),
-    "gp_group_candidates": (C.c_int, [vp, i64, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int,
+    "gp_group_candidates": (C.c_int, [vp, i64, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_int,
                                       C.c_int, vp, vp, C.c_int, vp]),
     "gp_audit": (C.c_int, [C.POINTER(AssignArgs), vp, vp]),
     "gp_fold_workspace_bytes": (C.c_int, [i64, i64, i64, C.c_int, C.POINTER(sz)]),

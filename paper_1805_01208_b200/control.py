@@ -109,6 +109,18 @@ def sample_schedule(n: int, init_sample: int) -> list[int]:
     return [init_sample * 2**j for j in range(rounds)]
 
 
+def _f32_up(x):
+    x = np.asarray(x, dtype=np.float64)
+    f = x.astype(np.float32)
+    return np.where(f.astype(np.float64) < x, np.nextafter(f, np.float32(np.inf)), f)
+
+
+def _f32_down(x):
+    x = np.asarray(x, dtype=np.float64)
+    f = x.astype(np.float32)
+    return np.where(f.astype(np.float64) > x, np.nextafter(f, np.float32(-np.inf)), f)
+
+
 class BoundMaps:
     """Cumulative affine maps standing in for per-point eager relaxation.
 
@@ -150,6 +162,34 @@ class BoundMaps:
     @property
     def bound_err(self) -> float:
         return (4.0 * self.steps + 16.0) * 2.0 ** -52
+
+    def device_params(self):
+        """Float32 parameters of the device bound arithmetic, rounded outward.
+
+        Returns (ub_eval (k,4), ub_norm (k,4), lb_a, lb_b, lb_inva, lb_blo) with
+          ub <= fmaf_ru(ub~ >= 0 ? E.x : E.y, ub~, E.z)   (E = ub_eval[a])
+          lb >= max(fmaf_rd(lb_a, lb~, -lb_b), 0)
+        covering the composition error of the float64 maps (bound_err), and the
+        normalisation constants (1/S up/down, T down, 1/A down, B down).
+        """
+        e = self.bound_err
+        S, T = self.ub_scale, self.ub_shift
+        k = S.shape[0]
+        ev = np.zeros((k, 4), dtype=np.float32)
+        ev[:, 0] = _f32_up(S * (1.0 + e))
+        ev[:, 1] = _f32_down(S * (1.0 - e))
+        ev[:, 2] = _f32_up(T * (1.0 + e))
+        nm = np.zeros((k, 4), dtype=np.float32)
+        inv = 1.0 / S
+        nm[:, 0] = _f32_up(np.nextafter(inv, np.inf))
+        nm[:, 1] = _f32_down(np.nextafter(inv, 0.0))
+        nm[:, 2] = _f32_down(T)
+        A, B = self.lb_scale, self.lb_shift
+        lb_a = float(_f32_down(np.array([A * (1.0 - e)]))[0])
+        lb_b = float(_f32_up(np.array([B * (1.0 + e)]))[0])
+        lb_inva = float(_f32_down(np.array([np.nextafter(1.0 / A, 0.0)]))[0])
+        lb_blo = float(_f32_down(np.array([B]))[0])
+        return ev, nm, lb_a, lb_b, lb_inva, lb_blo
 
     def needs_rebase(self, scale_hint: float) -> bool:
         lim = 1e6

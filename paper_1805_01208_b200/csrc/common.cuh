@@ -73,20 +73,37 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 }
 __host__ __device__ __forceinline__ unsigned long long dkey_host_min() { return ~0ull; }
 
-// Lazily relaxed Hamerly bounds: ub = S[a]*ub~ + T[a] and
-// lb = max(A*lb~ - B, 0), evaluated with one directed rounding (FMA) and widened
-// by the host composition error err*(|S*ub~| + |T|) so cancellation near zero
-// can never make them unsound.
-__device__ __forceinline__ double ub_eval(double S, double u, double T, double err) {
-  double v = __fma_ru(S, u, T);
-  double mag = __dadd_ru(fabs(__dmul_ru(S, u)), fabs(T));
-  return __fma_ru(err, mag, v);
+// Lazily relaxed Hamerly bounds, evaluated in float32 with
+// outward rounding from host parameters that already include the composition
+// error margin (control.BoundMaps.device_params).
+__device__ __forceinline__ float ub_evalf(float4 E, float u) {
+  return __fmaf_ru(u >= 0.f ? E.x : E.y, u, E.z);
 }
-__device__ __forceinline__ double lb_eval(double A, double l, double B, double err) {
+__device__ __forceinline__ float lb_evalf(float A, float l, float B) {
   if (isinf(l)) return l;  // k == 1: no runner-up
-  double v = __fma_rd(A, l, -B);
-  double mag = __dadd_ru(__dmul_ru(A, l), B);
-  return fmax(__fma_rd(-err, mag, v), 0.0);
+  return fmaxf(__fmaf_rd(A, l, -B), 0.f);
+}
+// normalise fresh bounds (b rounded up, s rounded down) under the current maps
+__device__ __forceinline__ float ub_normf(float4 N, float b_up) {
+  const float num = __fsub_ru(b_up, N.z);
+  return __fmul_ru(num, num >= 0.f ? N.x : N.y);
+}
+__device__ __forceinline__ float lb_normf(float inva, float blo, float s_dn) {
+  if (isinf(s_dn)) return s_dn;
+  return __fmul_rd(__fadd_rd(s_dn, blo), inva);
+}
+
+// point i of an AoS coordinate array with point stride ldx
+template <int D>
+__device__ __forceinline__ void load_point(const double* X, int64_t ldx, int64_t i, double* out) {
+  if (D == 2 && ldx == 2) {
+    const double2 v = reinterpret_cast<const double2*>(X)[i];
+    out[0] = v.x;
+    out[1] = v.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[j] = X[i * ldx + j];
+  }
 }
 
 __device__ __forceinline__ double load_weight(const void* w, int wmode, int64_t i) {
@@ -96,9 +113,15 @@ __device__ __forceinline__ double load_weight(const void* w, int wmode, int64_t 
 }
 
 // Segment (of GP_SEGMENTS equal position ranges, ranksim.py:74-75) of a global
-// position: the largest s with floor(s*n/S) <= pos.
+// position: the largest s with floor(s*n/S) <= pos.  S is a power of two, so
+// the boundaries are (s*n) >> 8; a floating-point estimate is corrected with
+// exact integer checks (no 64-bit division).
 __device__ __forceinline__ int segment_of(int64_t pos, int64_t n) {
-  return (int)(((pos + 1) * (int64_t)GP_SEGMENTS - 1) / n);
+  int s = (int)((double)pos * ((double)GP_SEGMENTS / (double)n));
+  s = s < 0 ? 0 : (s > GP_SEGMENTS - 1 ? GP_SEGMENTS - 1 : s);
+  while (s > 0 && (((int64_t)s * n) >> 8) > pos) --s;
+  while (s < GP_SEGMENTS - 1 && (((int64_t)(s + 1) * n) >> 8) <= pos) ++s;
+  return s;
 }
 
 inline unsigned grid_for(int64_t work, int per_block, int cap = 1 << 30) {

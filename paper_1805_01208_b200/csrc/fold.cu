@@ -162,8 +162,10 @@ __global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const int32_t*
           bool in = i < re;
           wv[b] = in ? load_weight(f.w, f.wmode, i) : 0.0;
           if (!f.weights_only) {
+            if (in) load_point<D>(f.X, f.ldx, i, xv[b]);
+            else
 #pragma unroll
-            for (int j = 0; j < D; ++j) xv[b][j] = in ? f.X[j * f.ldx + i] : 0.0;
+              for (int j = 0; j < D; ++j) xv[b][j] = 0.0;
           }
         }
 #pragma unroll

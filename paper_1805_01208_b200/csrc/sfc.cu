@@ -190,7 +190,7 @@ __global__ void gather_points_kernel(const double* __restrict__ pts, int64_t sp,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t g = gids[i];
-    for (int j = 0; j < d; ++j) X[j * ldx + i] = pts[g * sp + j * sd];
+    for (int j = 0; j < d; ++j) X[i * ldx + j] = pts[g * sp + j * sd];
     if (wmode == GP_W_F32) ((float*)w_out)[i] = (float)w_in[g];
     else if (wmode == GP_W_F64) ((double*)w_out)[i] = w_in[g];
   }
@@ -200,7 +200,7 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, int64_t ldx, in
                                    const int64_t* __restrict__ pos, int k, double* rows) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < k)
-    for (int j = 0; j < d; ++j) rows[i * d + j] = X[j * ldx + pos[i]];
+    for (int j = 0; j < d; ++j) rows[i * d + j] = X[pos[i] * ldx + j];
 }
 
 // ------------------------------------------------------- K5 compaction

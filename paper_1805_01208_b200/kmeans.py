@@ -179,14 +179,15 @@ class _Hierarchy:
         """Candidate lists under the current centers and influences (every round)."""
         eng = self.eng
         d, k = eng.d, eng.settings.k
-        cen, infl = eng.centers_d.data_ptr(), eng.kstate.data_ptr()
+        cen = eng.centers_d.data_ptr()
+        i2lo, i2hi = eng.aargs.inv2_lo, eng.aargs.inv2_hi
         parent, pcount, pcap = None, None, 0
         if self.use_mega:
-            N.call("gp_group_candidates", self.mbox.data_ptr(), self.nm, d, k, cen, infl,
+            N.call("gp_group_candidates", self.mbox.data_ptr(), self.nm, d, k, cen, i2lo, i2hi,
                    None, None, 0, 0, self.mlist.data_ptr(), self.mcount.data_ptr(),
                    self.MEGA_CAP, eng.sh)
             parent, pcount, pcap = self.mlist.data_ptr(), self.mcount.data_ptr(), self.MEGA_CAP
-        N.call("gp_group_candidates", self.sbox.data_ptr(), self.ns, d, k, cen, infl,
+        N.call("gp_group_candidates", self.sbox.data_ptr(), self.ns, d, k, cen, i2lo, i2hi,
                parent, pcount, pcap, self.MEGA_SHIFT - self.SUPER_SHIFT,
                self.slist.data_ptr(), self.scount.data_ptr(), self.SUPER_CAP, eng.sh)
 
@@ -275,8 +276,8 @@ class DevicePartitioner:
                self.gids.data_ptr(), n, d * depth, ws.data_ptr(), wsb, sh)
         self.keys_sorted = keys_s if self.keep_keys else None
         del keys, gids, ws, keys_s
-        self.ldx = n
-        self.X = torch.empty((d, n), dtype=torch.float64, device=dev)
+        self.ldx = d
+        self.X = torch.empty((n, d), dtype=torch.float64, device=dev)  # AoS, SFC order
         self.W = None
         if w is not None:
             self.W = torch.empty(n, dtype=torch.float32 if self.wplan.mode == 1 else torch.float64,
@@ -314,9 +315,12 @@ class DevicePartitioner:
     def _alloc_state(self):
         n, k, d, dev = self.n, self.settings.k, self.d, self.device
         self.A = torch.full((n,), -1, dtype=torch.int32, device=dev)
-        self.UB = torch.full((n,), math.inf, dtype=torch.float64, device=dev)
-        self.LB = torch.zeros(n, dtype=torch.float64, device=dev)
-        self.kstate = torch.empty(3 * k, dtype=torch.float64, device=dev)  # infl | ubS | ubT
+        # (ub~, lb~) float32 pairs: ub~ = +inf (unassigned), lb~ = 0 (kmeans.py:146-147)
+        self.UBLB = torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        self.UBLB[:, 0] = math.inf
+        # infl | inv2_lo | inv2_hi (float64) and ub_eval | ub_norm (float32, k x 4 each)
+        self.kstate = torch.empty(3 * k, dtype=torch.float64, device=dev)
+        self.kmaps = torch.empty(8 * k, dtype=torch.float32, device=dev)
         self.red = torch.zeros(k + 3, dtype=torch.int64, device=dev)      # block_w | counters
         self.audit_out = torch.zeros(3, dtype=torch.int64, device=dev)
         self.fold_out = torch.empty(k * (d + 3), dtype=torch.float64, device=dev)
@@ -327,10 +331,12 @@ class DevicePartitioner:
         a.wmode = self.wplan.mode if self.W is not None else 0
         a.w = _ptr(self.W)
         a.wscale = self.wplan.scale
-        a.a, a.ub, a.lb = self.A.data_ptr(), self.UB.data_ptr(), self.LB.data_ptr()
+        a.a, a.ublb = self.A.data_ptr(), self.UBLB.data_ptr()
         a.centers = self.centers_d.data_ptr()
         base = self.kstate.data_ptr()
-        a.infl, a.ub_scale, a.ub_shift = base, base + 8 * k, base + 16 * k
+        a.infl, a.inv2_lo, a.inv2_hi = base, base + 8 * k, base + 16 * k
+        mb = self.kmaps.data_ptr()
+        a.ub_eval, a.ub_norm = mb, mb + 16 * k
         a.block_w = self.red.data_ptr()
         a.counters = self.red.data_ptr() + 8 * k
         awb = N.size_query("gp_assign_workspace_bytes", n)
@@ -351,11 +357,15 @@ class DevicePartitioner:
 
     def _push_kstate(self, infl, maps: BoundMaps):
         k = self.settings.k
-        host = np.concatenate([infl, maps.ub_scale, maps.ub_shift])
+        inv2 = 1.0 / (infl * infl)
+        inv2_lo = np.nextafter(np.nextafter(inv2, 0.0), 0.0)   # 2 ulps cover the 2 roundings
+        inv2_hi = np.nextafter(np.nextafter(inv2, np.inf), np.inf)
+        host = np.concatenate([infl, inv2_lo, inv2_hi])
         self.kstate.copy_(torch.from_numpy(host), non_blocking=False)
-        self.aargs.lb_scale = maps.lb_scale
-        self.aargs.lb_shift = maps.lb_shift
-        self.aargs.bound_err = maps.bound_err
+        ev, nm, la, lb, linv, lblo = maps.device_params()
+        self.kmaps.copy_(torch.from_numpy(np.concatenate([ev.ravel(), nm.ravel()])))
+        a = self.aargs
+        a.lb_a, a.lb_b, a.lb_inva, a.lb_blo = la, lb, linv, lblo
         del k
 
     def _set_active(self, size):
@@ -534,7 +544,7 @@ class DevicePartitioner:
 
     def release(self):
         """Drop every n-sized device buffer (the caller keeps only the result)."""
-        for name in ("X", "W", "A", "A_fb", "UB", "LB", "gids", "rank_sfc", "active_idx",
+        for name in ("X", "W", "A", "A_fb", "UBLB", "gids", "rank_sfc", "active_idx",
                      "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier"):
             if hasattr(self, name):
                 setattr(self, name, None)

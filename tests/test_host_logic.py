@@ -69,17 +69,27 @@ def test_relax_bounds_identity_and_floor():
     assert out.lower[0] == 0.0 and out.upper[0] == pytest.approx(11.0, rel=1e-9)
 
 
+def _f32(x):
+    return np.asarray(x, dtype=np.float32)
+
+
 def test_lazy_bound_maps_are_sound_against_eager_relaxation():
-    """Composed maps never produce a tighter bound than the reference's eager relax."""
+    """Device float32 bound arithmetic (emulated in float64 on the outward-rounded
+    parameters) never gives a tighter bound than the reference's eager relaxation."""
     rng = np.random.default_rng(3)
     k, m = 7, 400
     maps = BoundMaps(k)
     a = rng.integers(0, k, m)
-    best = rng.uniform(0.01, 1.0, m)
+    best = rng.uniform(0.0, 1.0, m)
+    best[:20] = 0.0  # points sitting on their center (cancellation case)
     second = best + rng.uniform(0.0, 1.0, m)
     ub_eager, lb_eager = best.copy(), second.copy()
-    ub_t = (best - maps.ub_shift[a]) / maps.ub_scale[a]
-    lb_t = (second + maps.lb_shift) / maps.lb_scale
+    ev, nm, la, lb, linv, lblo = maps.device_params()
+    num = best - nm[a, 2].astype(np.float64)
+    ub_t = num * np.where(num >= 0, nm[a, 0], nm[a, 1]).astype(np.float64)
+    ub_t = np.nextafter(ub_t.astype(np.float32), np.float32(np.inf)).astype(np.float64)
+    lb_t = (second + lblo) * linv
+    lb_t = np.nextafter(lb_t.astype(np.float32), np.float32(-np.inf)).astype(np.float64)
     infl = np.ones(k)
     for step in range(300):
         new = infl * rng.uniform(0.95, 1.05, k)
@@ -88,15 +98,14 @@ def test_lazy_bound_maps_are_sound_against_eager_relaxation():
         ub_eager, lb_eager = b2.upper, b2.lower
         maps.relax(infl, new, moves)
         infl = new
-        e = maps.bound_err
-        ub_lazy = maps.ub_scale[a] * ub_t + maps.ub_shift[a]
-        ub_lazy += e * (np.abs(maps.ub_scale[a] * ub_t) + maps.ub_shift[a])
-        lb_lazy = maps.lb_scale * lb_t - maps.lb_shift
-        lb_lazy = np.maximum(lb_lazy - e * (maps.lb_scale * lb_t + maps.lb_shift), 0.0)
-        assert np.all(ub_lazy >= ub_eager * (1 - 1e-13))
-        assert np.all(lb_lazy <= lb_eager * (1 + 1e-13) + 1e-300)
-        # and nearly as tight
-        assert np.all(ub_lazy <= ub_eager * (1 + 1e-9))
+        ev, nm, la, lb, linv, lblo = maps.device_params()
+        E = ev[a].astype(np.float64)
+        ub_lazy = np.where(ub_t >= 0, E[:, 0], E[:, 1]) * ub_t + E[:, 2]
+        lb_lazy = np.maximum(la * lb_t - lb, 0.0)
+        assert np.all(ub_lazy >= ub_eager * (1 - 1e-12))
+        assert np.all(lb_lazy <= lb_eager * (1 + 1e-12) + 1e-300)
+        # and still tight to float32 precision
+        assert np.all(ub_lazy <= ub_eager * (1 + 1e-5) + 1e-6)
 
 
 def test_sample_schedule():

@@ -1,0 +1,53 @@
+"""Per-kernel device-time table of one partition (torch.profiler / CUPTI, no replay).
+
+    python tools/kprof.py C5 [--warm]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1805_01208_b200 import KMeansSettings  # noqa: E402
+from paper_1805_01208_b200.kmeans import _Timer, partition_device  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+dev = torch.device("cuda")
+c, pts_d, w_d, _ = bench.device_workload(cfg, dev)
+s = KMeansSettings(k=c["k"], epsilon=c["epsilon"], seed=0)
+partition_device(pts_d, w_d, s, device=dev)  # warm
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    out, stats = partition_device(pts_d, w_d, s, device=dev)
+    torch.cuda.synchronize()
+rows = {}
+for e in prof.events():
+    if e.device_type.name != "CUDA":
+        continue
+    r = rows.setdefault(e.name[:70], [0, 0.0])
+    r[0] += 1
+    r[1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+tot = sum(v[1] for v in rows.values())
+print(f"{'kernel':72s} {'calls':>6s} {'ms':>10s} {'%':>6s}")
+for k, v in sorted(rows.items(), key=lambda x: -x[1][1])[:25]:
+    print(f"{k:72s} {v[0]:6d} {v[1] / 1e3:10.2f} {100 * v[1] / tot:6.1f}")
+print("device total ms", tot / 1e3, "rounds", sum(r.balance_rounds for r in stats.iterations),
+      "iterations", len(stats.iterations))
+print("phase active rounds scanned/round evals/scanned")
+for r in stats.iterations[::4] + stats.iterations[-3:]:
+    sc = r.total_decisions - r.skip_decisions
+    print(r.phase, r.active_points, r.balance_rounds, sc // max(r.balance_rounds, 1),
+          round(r.distance_evals / max(sc, 1), 2))
+
+t = _Timer()
+out, stats = partition_device(pts_d, w_d, s, device=dev, timer=t)
+torch.cuda.synchronize()
+ms = [a.elapsed_time(b) for a, b in t.events]
+full = [(m, r) for m, r in zip(ms, t.rounds) if r[0] == c["n"]]
+samp = [(m, r) for m, r in zip(ms, t.rounds) if r[0] != c["n"]]
+print("assign ms: sample %.1f (%d rounds), full %.1f (%d rounds, %.3f ms/round, scanned/round %.0f)"
+      % (sum(m for m, _ in samp), len(samp), sum(m for m, _ in full), len(full),
+         sum(m for m, _ in full) / max(len(full), 1),
+         sum(r[1] for _, r in full) / max(len(full), 1)))
