@@ -216,6 +216,9 @@ typedef struct gp_fold_args {
 int gp_fold_workspace_bytes(int64_t n_local, int64_t pos0, int64_t n_global, int k,
                             size_t* bytes);
 int gp_movement_fold(const gp_fold_args* args, void* stream);
+/* Debugging aid (synchronises the device): out[4] = {runs, work cursor, valid runs,
+ * pairs} of the last gp_movement_fold call. */
+int gp_fold_stats(int64_t* out);
 
 /* K8  bound audit (kmeans.py:347-365): brute-force n x k recheck of the
  * bound contracts for the active points; out[3] += {audited, violations,

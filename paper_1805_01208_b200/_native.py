@@ -71,6 +71,7 @@ _SIGS = {
     "gp_audit": (C.c_int, [C.POINTER(AssignArgs), vp, vp]),
     "gp_fold_workspace_bytes": (C.c_int, [i64, i64, i64, C.c_int, C.POINTER(sz)]),
     "gp_movement_fold": (C.c_int, [C.POINTER(FoldArgs), vp]),
+    "gp_fold_stats": (C.c_int, [vp]),
     "gp_scatter_by_gid": (C.c_int, [vp, vp, i64, vp, vp]),
     "gp_gather_ranks": (C.c_int, [vp, vp, i64, vp, vp]),
 }

@@ -18,6 +18,7 @@
 //              by all lanes of the chunk;
 //   combine  : per block, fold the pair partials in segment order.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
@@ -33,7 +34,7 @@ constexpr int FB = 4;       // chunks of 32 positions prefetched per batch
 struct FoldLayout {
   int64_t s0, nseg, cells, cap, pcap;
   size_t off_flags, off_starts, off_rkey, off_skey, off_sidx, off_ridx, off_pbeg, off_slot,
-      off_out, off_counters, off_cub, cub_bytes, total;
+      off_out, off_counters, off_cub, cub_bytes, off_rpre, off_spos, total;
 };
 
 static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k) {
@@ -45,7 +46,9 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   L.cells = L.nseg * k;
   L.cap = n_local > 0 ? n_local : 1;
   L.pcap = L.cells < L.cap ? L.cells : L.cap;  // pairs <= min(segments x blocks, runs)
-  size_t b1 = 0, b2 = 0;
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b3, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)L.cap + 1);
   cub::DeviceSelect::Flagged(nullptr, b1, cub::CountingInputIterator<int32_t>(0),
                              (const uint8_t*)nullptr, (int32_t*)nullptr, (int64_t*)nullptr,
                              (int)L.cap);
@@ -53,6 +56,7 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   cub::DoubleBuffer<int32_t> vb(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, b2, kb, vb, (int)L.cap, 0, 32);
   L.cub_bytes = b1 > b2 ? b1 : b2;
+  if (b3 > L.cub_bytes) L.cub_bytes = b3;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   size_t o = 0;
   L.off_flags = o; o = al(o + L.cap);
@@ -66,6 +70,8 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   L.off_out = o; o = al(o + L.pcap * (MAXCOL + 1) * sizeof(double));
   L.off_counters = o; o = al(o + 8 * sizeof(int64_t));
   L.off_cub = o; o = al(o + L.cub_bytes);
+  L.off_rpre = o; o = al(o + (L.cap + 1) * 8);
+  L.off_spos = o; o = al(o + L.cap * 4);
   L.total = o;
   return L;
 }
@@ -76,14 +82,41 @@ __device__ __forceinline__ int32_t fold_key(const int32_t* a, int64_t i, int64_t
   return c >= 0 ? (int32_t)((segment_of(pos0 + i, n_global) - s0) * k + c) : -1;
 }
 
-// flag every position whose key differs from its predecessor's (run starts)
+// flag every position whose key differs from its predecessor's (run starts);
+// each thread handles MK consecutive positions with one segment computation
+constexpr int MK = 8;
 __global__ void fold_mark(const int32_t* __restrict__ a, int64_t n_local, int64_t pos0,
                           int64_t n_global, int64_t s0, int k, uint8_t* __restrict__ flags) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_local;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t key = fold_key(a, i, pos0, n_global, s0, k);
-    int32_t prev = i > 0 ? fold_key(a, i - 1, pos0, n_global, s0, k) : -2;
-    flags[i] = key != prev;
+  const int64_t nt = (n_local + MK - 1) / MK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = t * MK;
+    int seg = segment_of(pos0 + i0, n_global);
+    int64_t next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * n_global >> 8) - pos0
+                                            : INT64_MAX;  // local position of the next segment
+    int prev_key = i0 > 0 ? fold_key(a, i0 - 1, pos0, n_global, s0, k) : -2;
+    uint8_t f[MK];
+#pragma unroll
+    for (int e = 0; e < MK; ++e) {
+      const int64_t i = i0 + e;
+      if (i >= n_local) break;
+      while (i >= next_b) {
+        ++seg;
+        next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * n_global >> 8) - pos0 : INT64_MAX;
+      }
+      const int c = a[i];
+      const int key = c >= 0 ? (int)((seg - s0) * k + c) : -1;
+      f[e] = key != prev_key;
+      prev_key = key;
+    }
+    if (i0 + MK <= n_local) {
+      uint2 v;
+      v.x = f[0] | (f[1] << 8) | (f[2] << 16) | ((unsigned)f[3] << 24);
+      v.y = f[4] | (f[5] << 8) | (f[6] << 16) | ((unsigned)f[7] << 24);
+      *reinterpret_cast<uint2*>(flags + i0) = v;
+    } else {
+      for (int e = 0; i0 + e < n_local; ++e) flags[i0 + e] = f[e];
+    }
   }
 }
 
@@ -115,6 +148,37 @@ __global__ void fold_pair_flags(const uint32_t* __restrict__ skey, int64_t R,
     flags[j] = j < V && (j == 0 || skey[j] != skey[j - 1]);
 }
 
+// length of the j-th sorted run (valid runs only; 0 beyond)
+__global__ void fold_run_len(const int32_t* __restrict__ starts, const int32_t* __restrict__ sidx,
+                             int64_t R, const int64_t* counters, int64_t* __restrict__ len) {
+  const int64_t V = counters[2];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= R;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t l = 0;
+    if (j < V) {
+      const int r = sidx[j];
+      l = starts[r + 1] - starts[r];
+    }
+    len[j] = l;
+  }
+}
+
+// sorted positions: every valid position, grouped by pair, in position order
+// within the pair (one warp per sorted run)
+__global__ void fold_expand(const int32_t* __restrict__ starts, const int32_t* __restrict__ sidx,
+                            const int64_t* __restrict__ pre, const int64_t* counters,
+                            int32_t* __restrict__ spos) {
+  const int64_t V = counters[2];
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; j < V; j += nw) {
+    const int r = sidx[j];
+    const int32_t b = starts[r], e = starts[r + 1];
+    const int64_t o = pre[j];
+    for (int32_t t = lane; t < e - b; t += 32) spos[o + t] = b + t;
+  }
+}
+
 __global__ void fold_slots(const uint32_t* __restrict__ skey, int32_t* __restrict__ pbeg,
                            const int64_t* counters, int32_t* __restrict__ slot) {
   const int64_t P = counters[3];
@@ -124,13 +188,32 @@ __global__ void fold_slots(const uint32_t* __restrict__ skey, int32_t* __restric
     slot[skey[pbeg[p]]] = (int32_t)p;
 }
 
-// One warp per (segment, block) pair: its runs in position order, each run in
-// batches of FB chunks of 32 positions whose loads are all issued before any
-// value is consumed; lane j then folds column j over the batch in order.
+// One warp per (segment, block) pair: its positions (contiguous in spos, in
+// position order) in batches of FB*32; the loads of batch b+1 are issued before
+// batch b is folded, so the serial fold (lane j folds column j) overlaps them.
 template <int D>
-__global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const int32_t* __restrict__ starts,
+__device__ __forceinline__ void fold_load(const gp_fold_args& f, const int32_t* spos, int64_t v0,
+                                          int64_t v1, int lane, double (&xv)[FB][D],
+                                          double (&wv)[FB]) {
+#pragma unroll
+  for (int b = 0; b < FB; ++b) {
+    const int64_t v = v0 + b * 32 + lane;
+    const bool in = v < v1;
+    const int i = in ? spos[v] : 0;
+    wv[b] = in ? load_weight(f.w, f.wmode, i) : 0.0;
+    if (!f.weights_only) {
+      if (in) load_point<D>(f.X, f.ldx, i, xv[b]);
+      else
+#pragma unroll
+        for (int j = 0; j < D; ++j) xv[b][j] = 0.0;
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const int32_t* __restrict__ spos,
+                                                  const int64_t* __restrict__ pre,
                                                   const uint32_t* __restrict__ skey,
-                                                  const int32_t* __restrict__ sidx,
                                                   const int32_t* __restrict__ pbeg,
                                                   int64_t* counters, double* __restrict__ out) {
   __shared__ double sm[FT / 32][MAXCOL][FB * 32 + 1];
@@ -144,6 +227,7 @@ __global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const int32_t*
     if (pi >= npairs) break;
     const int j0 = pbeg[pi], j1 = pbeg[pi + 1];
     const int c = (int)(skey[j0] % (uint32_t)f.k);
+    const int64_t v0 = pre[j0], v1 = pre[j1];
     double cold[D];
     if (!f.weights_only) {
 #pragma unroll
@@ -151,55 +235,42 @@ __global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const int32_t*
     }
     double acc = 0.0;  // lane j < ncols folds column j; bincount starts from 0.0
     double ext = 0.0;
-    for (int jr = j0; jr < j1; ++jr) {
-      const int r = sidx[jr];
-      const int64_t rb = starts[r], re = starts[r + 1];  // every position in [rb, re) is block c
-      for (int64_t base = rb; base < re; base += FB * 32) {
-        double xv[FB][D], wv[FB];
+    double xv[FB][D], wv[FB];
+    fold_load<D>(f, spos, v0, v1, lane, xv, wv);
+    for (int64_t base = v0; base < v1; base += FB * 32) {
+      // stage the current batch, then issue the next batch's loads
 #pragma unroll
-        for (int b = 0; b < FB; ++b) {
-          int64_t i = base + b * 32 + lane;
-          bool in = i < re;
-          wv[b] = in ? load_weight(f.w, f.wmode, i) : 0.0;
-          if (!f.weights_only) {
-            if (in) load_point<D>(f.X, f.ldx, i, xv[b]);
-            else
+      for (int b = 0; b < FB; ++b) {
+        const int slot = b * 32 + lane;
+        const bool in = base + slot < v1;
+        if (f.weights_only) {
+          sm[warp][0][slot] = wv[b];
+        } else {
+          double diff[D];
 #pragma unroll
-              for (int j = 0; j < D; ++j) xv[b][j] = 0.0;
+          for (int j = 0; j < D; ++j) {
+            sm[warp][j][slot] = __dmul_rn(xv[b][j], wv[b]);  // wx = points * weights[:, None]
+            diff[j] = __dsub_rn(xv[b][j], cold[j]);
           }
+          const double sq = sqnorm_rn(diff, D, f.order3);
+          sm[warp][D][slot] = wv[b];
+          sm[warp][D + 1][slot] = __dmul_rn(sq, wv[b]);
+          if (in) ext = fmax(ext, __dsqrt_rn(sq));
         }
-#pragma unroll
-        for (int b = 0; b < FB; ++b) {
-          const int slot = b * 32 + lane;
-          const bool in = base + slot < re;
-          if (f.weights_only) {
-            sm[warp][0][slot] = wv[b];
-          } else {
-            double diff[D];
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-              sm[warp][j][slot] = __dmul_rn(xv[b][j], wv[b]);  // wx = points * weights[:, None]
-              diff[j] = __dsub_rn(xv[b][j], cold[j]);
-            }
-            double sq = sqnorm_rn(diff, D, f.order3);
-            sm[warp][D][slot] = wv[b];
-            sm[warp][D + 1][slot] = __dmul_rn(sq, wv[b]);
-            if (in) ext = fmax(ext, __dsqrt_rn(sq));
-          }
-        }
-        __syncwarp();
-        const int cnt = (int)min((int64_t)(FB * 32), re - base);
-        if (lane < ncols) {
-          const double* col = sm[warp][lane];
-          if (cnt == FB * 32) {
-#pragma unroll 32
-            for (int t = 0; t < FB * 32; ++t) acc = __dadd_rn(acc, col[t]);
-          } else {
-            for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, col[t]);
-          }
-        }
-        __syncwarp();
       }
+      __syncwarp();
+      if (base + FB * 32 < v1) fold_load<D>(f, spos, base + FB * 32, v1, lane, xv, wv);
+      const int cnt = (int)min((int64_t)(FB * 32), v1 - base);
+      if (lane < ncols) {
+        const double* col = sm[warp][lane];
+        if (cnt == FB * 32) {
+#pragma unroll 32
+          for (int t = 0; t < FB * 32; ++t) acc = __dadd_rn(acc, col[t]);
+        } else {
+          for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, col[t]);
+        }
+      }
+      __syncwarp();
     }
     for (int o = 16; o; o >>= 1) ext = fmax(ext, __shfl_xor_sync(FULL, ext, o));
     double* po = out + pi * (MAXCOL + 1);
@@ -250,7 +321,17 @@ __global__ void fold_combine(gp_fold_args f, const int32_t* __restrict__ slot, i
 
 using namespace gp;
 
+static int64_t* g_last_counters = nullptr;
+
 extern "C" {
+
+int gp_fold_stats(int64_t* out) {
+  // debugging aid: {runs, cursor, valid runs, pairs} of the last gp_movement_fold (syncs)
+  if (!g_last_counters) return GP_ERR_INVALID;
+  GP_CUDA(cudaDeviceSynchronize());
+  GP_CUDA(cudaMemcpy(out, g_last_counters, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return GP_OK;
+}
 
 int gp_fold_workspace_bytes(int64_t n_local, int64_t pos0, int64_t n_global, int k,
                             size_t* bytes) {
@@ -282,6 +363,9 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
   int32_t* slot = (int32_t*)(ws + L.off_slot);
   double* out = (double*)(ws + L.off_out);
   int64_t* counters = (int64_t*)(ws + L.off_counters);
+  int64_t* rpre = (int64_t*)(ws + L.off_rpre);
+  int32_t* spos = (int32_t*)(ws + L.off_spos);
+  g_last_counters = counters;
   void* cub_tmp = ws + L.off_cub;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -291,7 +375,7 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
   GP_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(int64_t), s));
   GP_CUDA(cudaMemsetAsync(slot, 0xff, L.cells * sizeof(int32_t), s));
   if (n > 0) {
-    fold_mark<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(f->a, n, f->pos0, f->n_global, L.s0,
+    fold_mark<<<grid_for((n + MK - 1) / MK, 256, sms * 16), 256, 0, s>>>(f->a, n, f->pos0, f->n_global, L.s0,
                                                           f->k, flags);
     size_t b = L.cub_bytes;
     GP_CUDA(cub::DeviceSelect::Flagged(cub_tmp, b, cub::CountingInputIterator<int32_t>(0), flags,
@@ -313,12 +397,18 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     GP_CUDA(cub::DeviceSelect::Flagged(cub_tmp, b, cub::CountingInputIterator<int32_t>(0), flags,
                                        pbeg, counters + 3, (int)R, s));
     fold_slots<<<grid_for(R, 256, sms * 8), 256, 0, s>>>(skey, pbeg, counters, slot);
+    // positions grouped by pair: prefix of the sorted run lengths, then expansion
+    fold_run_len<<<grid_for(R + 1, 256, sms * 8), 256, 0, s>>>(starts, sidx, R, counters, rpre);
+    b = L.cub_bytes;
+    GP_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, b, rpre, rpre, (int)(R + 1), s));
+    fold_expand<<<grid_for(R * 32, 256, sms * 16), 256, 0, s>>>(starts, sidx, rpre, counters,
+                                                                spos);
   }
   if (f->d == 2) {
-    fold_kernel<2><<<sms * 6, FT, 0, s>>>(*f, starts, skey, sidx, pbeg, counters, out);
+    fold_kernel<2><<<sms * 6, FT, 0, s>>>(*f, spos, rpre, skey, pbeg, counters, out);
     fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   } else {
-    fold_kernel<3><<<sms * 6, FT, 0, s>>>(*f, starts, skey, sidx, pbeg, counters, out);
+    fold_kernel<3><<<sms * 6, FT, 0, s>>>(*f, spos, rpre, skey, pbeg, counters, out);
     fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   }
   return check_launch("movement_fold");

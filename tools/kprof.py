@@ -51,3 +51,9 @@ print("assign ms: sample %.1f (%d rounds), full %.1f (%d rounds, %.3f ms/round, 
       % (sum(m for m, _ in samp), len(samp), sum(m for m, _ in full), len(full),
          sum(m for m, _ in full) / max(len(full), 1),
          sum(r[1] for _, r in full) / max(len(full), 1)))
+
+import numpy as np  # noqa: E402
+from paper_1805_01208_b200 import _native as N  # noqa: E402
+st = np.zeros(4, dtype=np.int64)
+N.lib.gp_fold_stats(st.ctypes.data)
+print("last fold: runs", st[0], "valid runs", st[2], "pairs", st[3])
