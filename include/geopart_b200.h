@@ -95,6 +95,17 @@ int gp_compact_workspace_bytes(int64_t n, size_t* bytes);
 int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx,
                       int64_t* count, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Dense view of a sample phase's active entries (the ~20 balance rounds of one
+ * movement iteration then stream contiguous arrays instead of gathering through
+ * the active list): gp_gather_state copies A, UBLB (float pairs), X (AoS, d
+ * columns) and W (wbytes per point, 0 = none) of list[0..m) into dense arrays;
+ * gp_scatter_state writes A and UBLB back. */
+int gp_gather_state(const int32_t* list, int64_t m, int d, const int32_t* a, const float* ublb,
+                    const double* X, const void* w, int wbytes, int32_t* a_out, float* ublb_out,
+                    double* X_out, void* w_out, void* stream);
+int gp_scatter_state(const int32_t* list, int64_t m, const int32_t* a_dense,
+                     const float* ublb_dense, int32_t* a, float* ublb, void* stream);
+
 /* K5b warm-up sample order, bit-exact with numpy: rank[perm[t]] = t for
  * perm = numpy.random.default_rng(seed).permutation(n) (kmeans.py:564-567).
  * pcg_state is a HOST array {state_hi, state_lo, inc_hi, inc_lo} of the
@@ -154,6 +165,19 @@ typedef struct gp_assign_args {
   /* scratch of gp_assign_workspace_bytes(m) bytes (filter -> scan hand-off) */
   void* workspace;
   size_t workspace_bytes;
+  /* scan unit = scan_regions x 256 consecutive entries (1..4; 0 = automatic).
+   * Dense (full-phase) lists want 4, sparse warm-up samples 1. */
+  int32_t scan_regions;
+  /* uniform grid over the centers (built on the host per movement iteration):
+   * cell (i0,i1[,i2]) covers [lo + i*h, lo + (i+1)*h); its centers are
+   * grid_items[grid_start[cell] .. grid_start[cell+1]).  Used for scan units whose
+   * candidate set overflows (sparse warm-up samples).  grid_n = 0: no grid. */
+  int32_t grid_n;
+  const int32_t* grid_start;
+  const int32_t* grid_items;
+  double grid_lo[3];
+  double grid_h;
+  double inv2_min;        /* lower bound of min_c 1/infl_c^2 */
 } gp_assign_args;
 int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);

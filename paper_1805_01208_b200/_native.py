@@ -32,7 +32,9 @@ class AssignArgs(C.Structure):
         ("ub_norm", vp), ("lb_a", C.c_float), ("lb_b", C.c_float), ("lb_inva", C.c_float),
         ("lb_blo", C.c_float), ("block_w", vp), ("counters", vp),
         ("group_list", vp), ("group_count", vp), ("group_cap", i32), ("group_shift", i32),
-        ("workspace", vp), ("workspace_bytes", sz),
+        ("workspace", vp), ("workspace_bytes", sz), ("scan_regions", i32), ("grid_n", i32),
+        ("grid_start", vp), ("grid_items", vp), ("grid_lo", f64 * 3), ("grid_h", f64),
+        ("inv2_min", f64),
     ]
 
 
@@ -73,6 +75,9 @@ _SIGS = {
     "gp_movement_fold": (C.c_int, [C.POINTER(FoldArgs), vp]),
     "gp_fold_stats": (C.c_int, [vp]),
     "gp_scatter_by_gid": (C.c_int, [vp, vp, i64, vp, vp]),
+    "gp_gather_state": (C.c_int, [vp, i64, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp,
+                                  vp]),
+    "gp_scatter_state": (C.c_int, [vp, i64, vp, vp, vp, vp, vp]),
     "gp_gather_ranks": (C.c_int, [vp, vp, i64, vp, vp]),
 }
 
@@ -112,7 +117,7 @@ KERNELS_PER_CALL = {
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 3,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 16,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
-    "gp_group_candidates": 1, "gp_sample_ranks": 90,
+    "gp_group_candidates": 1, "gp_sample_ranks": 90, "gp_gather_state": 1, "gp_scatter_state": 1,
 }
 _launches = [0]
 

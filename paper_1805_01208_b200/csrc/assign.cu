@@ -253,6 +253,18 @@ __device__ __forceinline__ void stage(WarpCand<D>& W, int slot, int c, const gp_
   W.cid[slot] = c;
 }
 
+// keep the two smallest (q, idx) and the third smallest q when adding (t, it)
+__device__ __forceinline__ void top3_add(double& q1, int& i1, double& q2, int& i2, double& q3,
+                                         double t, int it) {
+  const bool l1 = t < q1 || (t == q1 && it < i1);
+  const bool l2 = !l1 && (t < q2 || (t == q2 && it < i2));
+  q3 = (l1 || l2) ? q2 : fmin(q3, t);
+  q2 = l1 ? q1 : (l2 ? t : q2);
+  i2 = l1 ? i1 : (l2 ? it : i2);
+  q1 = l1 ? t : q1;
+  i1 = l1 ? it : i1;
+}
+
 // squared distance / infl^2 (prefilter only; any rounding)
 template <int D>
 __device__ __forceinline__ double qdist(const double* x, const WarpCand<D>& W, int i) {
@@ -269,6 +281,108 @@ constexpr int SREG = 4;            // max filter regions per scan unit (runtime 
 constexpr double SEP = 1e-12;      // q separation above which no exact evaluation is needed
 constexpr float AP_HI_F = 1.0f + 2.4e-7f;  // margins of the sqrt(q)-derived float bounds
 constexpr float AP_LO_F = 1.0f - 2.4e-7f;
+
+// Visit the grid cells at Chebyshev distance r from cell (c0,c1,c2).
+template <int D, typename F>
+__device__ __forceinline__ void for_ring(const gp_assign_args& p, const int* cc, int r, F&& fn) {
+  const int G = p.grid_n;
+  if (D == 2) {
+    for (int i = cc[0] - r; i <= cc[0] + r; ++i) {
+      if (i < 0 || i >= G) continue;
+      const bool edge = i == cc[0] - r || i == cc[0] + r;
+      for (int j = cc[1] - r; j <= cc[1] + r; j += (edge || r == 0) ? 1 : 2 * r) {
+        if (j < 0 || j >= G) continue;
+        fn(i * G + j);
+      }
+    }
+  } else {
+    for (int i = cc[0] - r; i <= cc[0] + r; ++i) {
+      if (i < 0 || i >= G) continue;
+      for (int j = cc[1] - r; j <= cc[1] + r; ++j) {
+        if (j < 0 || j >= G) continue;
+        const bool face = i == cc[0] - r || i == cc[0] + r || j == cc[1] - r || j == cc[1] + r;
+        for (int l = cc[2] - r; l <= cc[2] + r; l += (face || r == 0) ? 1 : 2 * r) {
+          if (l < 0 || l >= G) continue;
+          fn((i * G + j) * G + l);
+        }
+      }
+    }
+  }
+}
+
+// Exact argmin (lowest index) and runner-up of one point by a ring walk over the
+// center grid: approximate q = d^2/infl^2 with the two smallest kept; a ring is
+// the last one once every farther cell is at least r*h away, i.e. q >= (r h)^2 *
+// inv2_min > q2 (1 + tol).  Near ties fall back to the reference's arithmetic on
+// every visited candidate within the tolerance.
+template <int D>
+__device__ void grid_point(const gp_assign_args& p, const double* x, int& bi, float& bestf,
+                           float& secondf, unsigned long long& nq) {
+  const int G = p.grid_n;
+  int cc[3] = {0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    int c = (int)floor((x[j] - p.grid_lo[j]) / p.grid_h);
+    cc[j] = c < 0 ? 0 : (c >= G ? G - 1 : c);
+  }
+  double q1 = INFINITY, q2 = INFINITY, q3 = INFINITY;
+  int i1 = 0x7fffffff, i2 = 0x7fffffff;
+  int rlast = 0;
+  for (int r = 0;; ++r) {
+    for_ring<D>(p, cc, r, [&](int cell) {
+      for (int t = p.grid_start[cell]; t < p.grid_start[cell + 1]; ++t) {
+        const int c = p.grid_items[t];
+        double s2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double dd = x[j] - p.centers[c * D + j];
+          s2 = fma(dd, dd, s2);
+        }
+        top3_add(q1, i1, q2, i2, q3, s2 * p.inv2_hi[c], c);
+        ++nq;
+      }
+    });
+    rlast = r;
+    bool covered = true;
+#pragma unroll
+    for (int j = 0; j < D; ++j) covered = covered && cc[j] - r <= 0 && cc[j] + r >= G - 1;
+    if (covered) break;
+    const double rh = (double)r * p.grid_h;
+    const double bound = __dmul_rd(__dmul_rd(rh, rh), p.inv2_min) * (1.0 - 1e-9);
+    if (bound > fma(q2, Q_TOL, q2)) break;
+  }
+  const double thr = fma(q2, Q_TOL, q2);
+  if (q3 > thr && q2 > fma(q1, SEP, q1)) {
+    bi = i1;
+    bestf = __fmul_ru(__fsqrt_ru(__double2float_ru(q1)), AP_HI_F);
+    secondf = i2 != 0x7fffffff ? __fmul_rd(__fsqrt_rd(__double2float_rd(q2)), AP_LO_F) : INFINITY;
+    return;
+  }
+  double best = INFINITY, second = INFINITY;
+  bi = 0x7fffffff;
+  for (int r = 0; r <= rlast; ++r) {
+    for_ring<D>(p, cc, r, [&](int cell) {
+      for (int t = p.grid_start[cell]; t < p.grid_start[cell + 1]; ++t) {
+        const int c = p.grid_items[t];
+        double s2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double dd = x[j] - p.centers[c * D + j];
+          s2 = fma(dd, dd, s2);
+        }
+        if (s2 * p.inv2_hi[c] <= thr) {
+          const double dist = effdist_rn<D>(x, p.centers + c * D, p.infl[c], p.order3);
+          const bool win = dist < best || (dist == best && c < bi);
+          second = win ? best : fmin(second, dist);
+          best = win ? dist : best;
+          bi = win ? c : bi;
+        }
+      }
+    });
+  }
+  bestf = __double2float_ru(best);
+  secondf = __double2float_rd(second);
+}
 
 template <int D, int WM>
 __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
@@ -404,6 +518,26 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
         W.order[r] = i;
       }
       __syncwarp();
+    }
+    if (overflow && p.grid_n > 0) {
+      // too many candidates for the staged set (sparse warm-up samples): every lane
+      // walks the center grid around its own point, ring by ring, until the ring's
+      // lower bound exceeds its runner-up
+      for (int v = lane; v < total_pts; v += 32) {
+        const int q = pos_of(v);
+        double x[D];
+        load_point<D>(p.X, p.ldx, q, x);
+        int bi;
+        float bestf, secondf;
+        unsigned long long nn = 0;
+        grid_point<D>(p, x, bi, bestf, secondf, nn);
+        nq += nn;
+        p.a[q] = bi;
+        store_bounds(p, q, bi, bestf, secondf);
+        cache_add(s_ckey, s_cval, p.block_w, bi, weight_units<WM>(p.w, q, wshift));
+      }
+      __syncwarp();
+      continue;
     }
     // ---- scan, one point per lane per pass
     for (int pb = 0; pb < total_pts; pb += 32) {
@@ -724,7 +858,8 @@ static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout
     g_sreg = e ? atoi(e) : -1;
   }
   // dense (full-phase) lists: 4 regions per scan unit; sparse sample lists: 1
-  int sreg = g_sreg > 0 ? g_sreg : (a->list ? 1 : SREG);
+  int sreg = g_sreg > 0 ? g_sreg
+                       : (a->scan_regions > 0 ? a->scan_regions : (a->list ? 1 : SREG));
   if (sreg > SREG) sreg = SREG;
   const int64_t wgroups = (L.nregions + sreg * (STH / 32) - 1) / (sreg * (STH / 32));
   if (a->d == 2) {

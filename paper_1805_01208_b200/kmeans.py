@@ -154,22 +154,23 @@ class _Hierarchy:
     def prepare(self, list_ptr, m):
         """Boxes of the groups of the current active list (once per active set)."""
         eng = self.eng
-        if self.key == (list_ptr, m):
+        key = (eng.aargs.X, list_ptr, m)
+        if self.key == key:
             return
-        self.key = (list_ptr, m)
+        self.key = key
         dev, d = eng.device, eng.d
         self.ns = max(1, (m + (1 << self.SUPER_SHIFT) - 1) >> self.SUPER_SHIFT)
         self.nm = max(1, (m + (1 << self.MEGA_SHIFT) - 1) >> self.MEGA_SHIFT)
         self.sbox = torch.empty(self.ns * 2 * d, dtype=torch.float64, device=dev)
         self.slist = torch.empty(self.ns * self.SUPER_CAP, dtype=torch.int32, device=dev)
         self.scount = torch.empty(self.ns, dtype=torch.int32, device=dev)
-        N.call("gp_group_boxes", eng.X.data_ptr(), eng.ldx, d, list_ptr, m, self.SUPER_SHIFT,
+        N.call("gp_group_boxes", eng.aargs.X, eng.ldx, d, list_ptr, m, self.SUPER_SHIFT,
                self.sbox.data_ptr(), eng.sh)
         if self.use_mega:
             self.mbox = torch.empty(self.nm * 2 * d, dtype=torch.float64, device=dev)
             self.mlist = torch.empty(self.nm * self.MEGA_CAP, dtype=torch.int32, device=dev)
             self.mcount = torch.empty(self.nm, dtype=torch.int32, device=dev)
-            N.call("gp_group_boxes", eng.X.data_ptr(), eng.ldx, d, list_ptr, m,
+            N.call("gp_group_boxes", eng.aargs.X, eng.ldx, d, list_ptr, m,
                    self.MEGA_SHIFT, self.mbox.data_ptr(), eng.sh)
         a = eng.aargs
         a.group_list, a.group_count = self.slist.data_ptr(), self.scount.data_ptr()
@@ -361,6 +362,7 @@ class DevicePartitioner:
         inv2_lo = np.nextafter(np.nextafter(inv2, 0.0), 0.0)   # 2 ulps cover the 2 roundings
         inv2_hi = np.nextafter(np.nextafter(inv2, np.inf), np.inf)
         host = np.concatenate([infl, inv2_lo, inv2_hi])
+        self.aargs.inv2_min = float(inv2_lo.min())
         self.kstate.copy_(torch.from_numpy(host), non_blocking=False)
         ev, nm, la, lb, linv, lblo = maps.device_params()
         self.kmaps.copy_(torch.from_numpy(np.concatenate([ev.ravel(), nm.ravel()])))
@@ -368,17 +370,79 @@ class DevicePartitioner:
         a.lb_a, a.lb_b, a.lb_inva, a.lb_blo = la, lb, linv, lblo
         del k
 
+    def _build_grid(self, centers: np.ndarray):
+        """Uniform grid over the point box holding the centers (k-sized host numpy),
+        walked by scan units whose candidate set overflows (gp_assign_args.grid_*)."""
+        k, d = centers.shape
+        lo = self.box.lo
+        ext = float((self.box.hi - self.box.lo).max())
+        G = int(np.ceil((k / 2.0) ** (1.0 / d)))
+        G = max(1, min(G, 1024 if d == 2 else 128))
+        h = ext / G * (1.0 + 1e-12) if ext > 0 else 1.0
+        cell = np.clip(np.floor((centers - lo) / h).astype(np.int64), 0, G - 1)
+        flat = cell[:, 0]
+        for j in range(1, d):
+            flat = flat * G + cell[:, j]
+        items = np.argsort(flat, kind="stable").astype(np.int32)
+        start = np.zeros(G ** d + 1, dtype=np.int32)
+        np.cumsum(np.bincount(flat, minlength=G ** d), out=start[1:])
+        self.grid_start = torch.from_numpy(start).to(self.device)
+        self.grid_items = torch.from_numpy(items).to(self.device)
+        a = self.aargs
+        a.grid_n, a.grid_h = G, h
+        a.grid_start, a.grid_items = self.grid_start.data_ptr(), self.grid_items.data_ptr()
+        for j in range(d):
+            a.grid_lo[j] = float(lo[j])
+
     def _set_active(self, size):
         m = self._set_active_list(size)
+        # (general-weight mode folds block weights from the full arrays every round)
+        if size is not None and self.wplan.exact:
+            self._enter_dense(m)
         if self.hier is not None:
             self.hier.prepare(self.aargs.list, m)
         return m
+
+    def _enter_dense(self, m):
+        """Sample phase: gather the active entries' state into dense arrays so the
+        ~20 balance rounds of this movement iteration stream contiguous memory."""
+        d, dev = self.d, self.device
+        if getattr(self, "dense_cap", 0) < m:
+            cap = max(self.sizes)
+            self.dense_cap = cap
+            self.A_d = torch.empty(cap, dtype=torch.int32, device=dev)
+            self.UBLB_d = torch.empty((cap, 2), dtype=torch.float32, device=dev)
+            self.X_d = torch.empty((cap, d), dtype=torch.float64, device=dev)
+            self.W_d = None if self.W is None else torch.empty(cap, dtype=self.W.dtype, device=dev)
+        wbytes = 0 if self.W is None else self.W.element_size()
+        N.call("gp_gather_state", self.active_idx.data_ptr(), m, d, self.A.data_ptr(),
+               self.UBLB.data_ptr(), self.X.data_ptr(), _ptr(self.W), wbytes,
+               self.A_d.data_ptr(), self.UBLB_d.data_ptr(), self.X_d.data_ptr(), _ptr(self.W_d),
+               self.sh)
+        a = self.aargs
+        a.X, a.a, a.ublb, a.w = (self.X_d.data_ptr(), self.A_d.data_ptr(),
+                                 self.UBLB_d.data_ptr(), _ptr(self.W_d))
+        a.list, a.m = None, m
+        self.dense_m = m
+
+    def _leave_dense(self):
+        """Write the dense sample state back and point the kernels at the full arrays."""
+        if not getattr(self, "dense_m", 0):
+            return
+        N.call("gp_scatter_state", self.active_idx.data_ptr(), self.dense_m, self.A_d.data_ptr(),
+               self.UBLB_d.data_ptr(), self.A.data_ptr(), self.UBLB.data_ptr(), self.sh)
+        a = self.aargs
+        a.X, a.a, a.ublb, a.w = (self.X.data_ptr(), self.A.data_ptr(), self.UBLB.data_ptr(),
+                                 _ptr(self.W))
+        self.dense_m = 0
 
     def _set_active_list(self, size):
         a = self.aargs
         if size is None:
             a.list, a.m = None, self.n
+            a.scan_regions = 4   # dense SFC-contiguous entries: 1024-entry scan units
             return self.n
+        a.scan_regions = 1       # sparse warm-up sample: 256-entry units
         N.call("gp_compact_active", self.rank_sfc.data_ptr(), self.n, size,
                self.active_idx.data_ptr(), self.active_cnt.data_ptr(),
                self.compact_ws.data_ptr(), self.compact_ws.numel(), self.sh)
@@ -424,6 +488,7 @@ class DevicePartitioner:
         last_move = np.zeros(k)
         maps = BoundMaps(k)
         self._push_kstate(infl, maps)
+        self._build_grid(centers)
         threshold = st.delta_threshold
         if threshold is None:
             threshold = 1e-4 * self.box.diagonal()
@@ -470,6 +535,7 @@ class DevicePartitioner:
                 infl = new_infl
                 self._push_kstate(infl, maps)
             info = BalanceInfo(rounds, final_imb, block_w, skips, decisions, evals, history)
+            self._leave_dense()
             if phase == "full" and info.imbalance <= st.epsilon:
                 if fallback is None:
                     self.A_fb = torch.empty_like(self.A)
@@ -513,6 +579,7 @@ class DevicePartitioner:
             infl = nxt
             last_move = moves
             self.centers_d.copy_(torch.from_numpy(np.ascontiguousarray(centers)))
+            self._build_grid(centers)
             if maps.needs_rebase(scale_hint / max(float(infl.min()), 1e-300)):
                 self._push_kstate(infl, maps)
                 a = self.aargs
@@ -544,8 +611,9 @@ class DevicePartitioner:
 
     def release(self):
         """Drop every n-sized device buffer (the caller keeps only the result)."""
-        for name in ("X", "W", "A", "A_fb", "UBLB", "gids", "rank_sfc", "active_idx",
-                     "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier"):
+        for name in ("X", "W", "A", "A_fb", "UBLB", "A_d", "UBLB_d", "X_d", "W_d", "gids", "rank_sfc", "active_idx",
+                     "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier", "grid_start",
+                     "grid_items"):
             if hasattr(self, name):
                 setattr(self, name, None)
 

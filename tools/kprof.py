@@ -57,3 +57,10 @@ from paper_1805_01208_b200 import _native as N  # noqa: E402
 st = np.zeros(4, dtype=np.int64)
 N.lib.gp_fold_stats(st.ctypes.data)
 print("last fold: runs", st[0], "valid runs", st[2], "pairs", st[3])
+by = {}
+for ms_, r in zip(ms, t.rounds):
+    e = by.setdefault(r[0], [0, 0.0, 0, 0])
+    e[0] += 1; e[1] += ms_; e[2] += r[1]; e[3] += r[2]
+print("active  rounds  ms  ms/round  scanned/round  qevals/scanned")
+for m_, e in sorted(by.items()):
+    print(m_, e[0], round(e[1], 1), round(e[1] / e[0], 3), e[2] // e[0], round(e[3] / max(e[2], 1), 1))
