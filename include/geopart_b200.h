@@ -148,10 +148,7 @@ typedef struct gp_assign_args {
    *   lb~ = (s + lb_blo) * lb_inva                 rounded down. */
   const float* ub_eval;   /* k x 4 */
   const float* ub_norm;   /* k x 4 */
-  float lb_a;
-  float lb_b;
-  float lb_inva;
-  float lb_blo;
+  const float* lb_par;    /* 4 floats: lb_a, lb_b, lb_inva, lb_blo */
   long long* block_w;     /* out: k exact block weights (units of 1/wscale), accumulated */
   unsigned long long* counters; /* out: [skips, decisions, evals], accumulated */
   /* optional hierarchical candidate source (gp_group_candidates): entry li of
@@ -201,6 +198,19 @@ int gp_group_candidates(const double* boxes, int64_t ngroups, int d, int k,
                         const int32_t* parent_list, const int32_t* parent_count, int parent_cap,
                         int parent_ratio_log2, int32_t* list, int32_t* count, int cap,
                         void* stream);
+
+/* Device-side bound-map bookkeeping (control.BoundMaps on the GPU): compose one
+ * relaxation (kmeans.py:208-239) old_infl -> new_infl with center moves `moves`
+ * (NULL = zero moves) into the cumulative maps `state` (S[k], T[k], then A, B,
+ * steps as doubles), unless it is the reference's identity early return, and
+ * derive every parameter the kernels read: inv2_lo/inv2_hi (k), ub_eval/ub_norm
+ * (k x 4 floats), lb_par (4 floats).  flags[0] is set to 1 when the maps should
+ * be re-based (gp_rebase_bounds + gp_reset_maps).  reset != 0 starts from
+ * identity maps (first call / after a rebase). */
+int gp_update_maps(const double* old_infl, const double* new_infl, const double* moves, int k,
+                   double* state, double* inv2_lo, double* inv2_hi, float* ub_eval,
+                   float* ub_norm, float* lb_par, int32_t* flags, int reset, double scale_hint,
+                   void* stream);
 
 /* Re-express every bound under identity maps (when the host's cumulative
  * maps drift out of range).  Same bound semantics as gp_assign_args. */

@@ -29,8 +29,7 @@ class AssignArgs(C.Structure):
         ("X", vp), ("ldx", i64), ("d", i32), ("k", i32), ("order3", i32), ("wmode", i32),
         ("w", vp), ("wscale", f64), ("list", vp), ("m", i64), ("a", vp), ("ublb", vp),
         ("centers", vp), ("infl", vp), ("inv2_lo", vp), ("inv2_hi", vp), ("ub_eval", vp),
-        ("ub_norm", vp), ("lb_a", C.c_float), ("lb_b", C.c_float), ("lb_inva", C.c_float),
-        ("lb_blo", C.c_float), ("block_w", vp), ("counters", vp),
+        ("ub_norm", vp), ("lb_par", vp), ("block_w", vp), ("counters", vp),
         ("group_list", vp), ("group_count", vp), ("group_cap", i32), ("group_shift", i32),
         ("workspace", vp), ("workspace_bytes", sz), ("scan_regions", i32), ("grid_n", i32),
         ("grid_start", vp), ("grid_items", vp), ("grid_lo", f64 * 3), ("grid_h", f64),
@@ -67,6 +66,8 @@ _SIGS = {
     "gp_assign_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_assign_round": (C.c_int, [C.POINTER(AssignArgs), vp]),
     "gp_rebase_bounds": (C.c_int, [C.POINTER(AssignArgs), vp]),
+    "gp_update_maps": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_int, f64,
+                                 vp]),
     "gp_group_boxes": (C.c_int, [vp, i64, C.c_int, vp, i64, C.c_int, vp, vp]),
     "gp_group_candidates": (C.c_int, [vp, i64, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_int,
                                       C.c_int, vp, vp, C.c_int, vp]),
@@ -117,7 +118,7 @@ KERNELS_PER_CALL = {
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 3,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 16,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
-    "gp_group_candidates": 1, "gp_sample_ranks": 90, "gp_gather_state": 1, "gp_scatter_state": 1,
+    "gp_group_candidates": 1, "gp_sample_ranks": 90, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 1,
 }
 _launches = [0]
 

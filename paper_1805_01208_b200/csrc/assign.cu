@@ -62,7 +62,7 @@ __device__ __forceinline__ void store_bounds(const gp_assign_args& p, int64_t q,
                                              float s_dn) {
   const float4 N = reinterpret_cast<const float4*>(p.ub_norm)[c];
   reinterpret_cast<float2*>(p.ublb)[q] =
-      make_float2(ub_normf(N, b_up), lb_normf(p.lb_inva, p.lb_blo, s_dn));
+      make_float2(ub_normf(N, b_up), lb_normf(p.lb_par[2], p.lb_par[3], s_dn));
 }
 
 __device__ __forceinline__ void cache_add(int* ckey, long long* cval, long long* global, int a,
@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
   __syncthreads();
   const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
   const int64_t cb = blockIdx.x * per, ce = min(nchunks, cb + per);
+  const float4 lbp = *reinterpret_cast<const float4*>(p.lb_par);
   unsigned long long nskip = 0;
   for (int64_t c = cb; c < ce; ++c) {
     const int64_t reg = c * (FCHUNK / WREG) + warp;
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
       const int ae = a[e];
       if (ae >= 0) {
         const float4 E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
-        skip = ub_evalf(E, ub[e]) < lb_evalf(p.lb_a, lb[e], p.lb_b);
+        skip = ub_evalf(E, ub[e]) < lb_evalf(lbp.x, lb[e], lbp.y);
       }
       if (!skip) {
         need |= 1u << e;
@@ -687,7 +688,7 @@ __global__ void audit_kernel(gp_assign_args p, unsigned long long* out) {
     }
     const double ub =
         a >= 0 ? ub_evalf(reinterpret_cast<const float4*>(p.ub_eval)[a], bnd.x) : INFINITY;
-    const double lb = lb_evalf(p.lb_a, bnd.y, p.lb_b);
+    const double lb = lb_evalf(p.lb_par[0], bnd.y, p.lb_par[1]);
     ++aud;
     if (a >= 0 && ub < own) ++viol;
     if (p.k > 1 && lb > m2) ++viol;
@@ -707,7 +708,7 @@ __global__ void rebase_kernel(gp_assign_args p) {
     // the host resets the maps to identity after this pass: store the values themselves
     const float ub = a >= 0 ? ub_evalf(reinterpret_cast<const float4*>(p.ub_eval)[a], bnd.x)
                             : bnd.x;
-    reinterpret_cast<float2*>(p.ublb)[q] = make_float2(ub, lb_evalf(p.lb_a, bnd.y, p.lb_b));
+    reinterpret_cast<float2*>(p.ublb)[q] = make_float2(ub, lb_evalf(p.lb_par[0], bnd.y, p.lb_par[1]));
   }
 }
 
@@ -825,6 +826,104 @@ __global__ void __launch_bounds__(256) group_candidates_kernel(
   if (threadIdx.x == 0) count[g] = s_n <= cap ? s_n : -1;
 }
 
+// ------------------------------------------------------------ bound maps
+// Mirror of control.BoundMaps.relax + device_params for one CTA.
+constexpr double UBS = 1.0 + 1e-12, LBS = 1.0 - 1e-12;
+
+__global__ void __launch_bounds__(1024) update_maps_kernel(
+    const double* __restrict__ old_infl, const double* __restrict__ new_infl,
+    const double* __restrict__ moves, int k, double* __restrict__ st,
+    double* __restrict__ inv2_lo, double* __restrict__ inv2_hi, float4* __restrict__ ub_eval,
+    float4* __restrict__ ub_norm, float* __restrict__ lb_par, int32_t* __restrict__ flags,
+    int reset, double scale_hint) {
+  __shared__ double s_min[32], s_max[32];
+  __shared__ int s_any[32];
+  double* S = st;
+  double* T = st + k;
+  double* ABs = st + 2 * k;  // A, B, steps
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // reductions: changed?, min ratio, max shift
+  double rmin = INFINITY, smax = 0.0;
+  int any = 0;
+  for (int c = tid; c < k; c += blockDim.x) {
+    const double mv = moves ? moves[c] : 0.0;
+    any |= (mv != 0.0) || (old_infl[c] != new_infl[c]);
+    rmin = fmin(rmin, old_infl[c] / new_infl[c]);
+    smax = fmax(smax, mv / new_infl[c]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    rmin = fmin(rmin, __shfl_xor_sync(FULL, rmin, o));
+    smax = fmax(smax, __shfl_xor_sync(FULL, smax, o));
+    any |= __shfl_xor_sync(FULL, any, o);
+  }
+  if (lane == 0) {
+    s_min[warp] = rmin;
+    s_max[warp] = smax;
+    s_any[warp] = any;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x / 32;
+    rmin = lane < nw ? s_min[lane] : INFINITY;
+    smax = lane < nw ? s_max[lane] : 0.0;
+    any = lane < nw ? s_any[lane] : 0;
+    for (int o = 16; o; o >>= 1) {
+      rmin = fmin(rmin, __shfl_xor_sync(FULL, rmin, o));
+      smax = fmax(smax, __shfl_xor_sync(FULL, smax, o));
+      any |= __shfl_xor_sync(FULL, any, o);
+    }
+    if (lane == 0) {
+      s_min[0] = rmin;
+      s_max[0] = smax;
+      s_any[0] = any;
+    }
+  }
+  __syncthreads();
+  rmin = s_min[0];
+  smax = s_max[0];
+  // relax_bounds' identity early return (kmeans.py:223-228)
+  const bool compose = !reset && s_any[0];
+  double A = reset ? 1.0 : ABs[0], B = reset ? 0.0 : ABs[1], steps = reset ? 0.0 : ABs[2];
+  if (compose) {
+    A = A * rmin * LBS;
+    B = (B * rmin + smax) * LBS;
+    steps += 1.0;
+  }
+  const double e = (4.0 * steps + 16.0) * 0x1p-52;
+  int out_of_range = 0;
+  for (int c = tid; c < k; c += blockDim.x) {
+    double Sc = reset ? 1.0 : S[c], Tc = reset ? 0.0 : T[c];
+    if (compose) {
+      const double r = old_infl[c] / new_infl[c];
+      const double sh = (moves ? moves[c] : 0.0) / new_infl[c];
+      Sc = Sc * r * UBS;
+      Tc = (Tc * r + sh) * UBS;
+    }
+    S[c] = Sc;
+    T[c] = Tc;
+    const double I = new_infl[c];
+    inv2_lo[c] = __ddiv_rd(1.0, __dmul_ru(I, I));
+    inv2_hi[c] = __ddiv_ru(1.0, __dmul_rd(I, I));
+    ub_eval[c] = make_float4(__double2float_ru(__dmul_ru(Sc, 1.0 + e)),
+                             __double2float_rd(__dmul_rd(Sc, 1.0 - e)),
+                             __double2float_ru(__dmul_ru(Tc, 1.0 + e)), 0.f);
+    ub_norm[c] = make_float4(__double2float_ru(__ddiv_ru(1.0, Sc)),
+                             __double2float_rd(__ddiv_rd(1.0, Sc)), __double2float_rd(Tc), 0.f);
+    out_of_range |= Sc < 1e-6 || Sc > 1e6 || Tc > 64.0 * scale_hint;
+  }
+  out_of_range = __syncthreads_or(out_of_range);
+  if (tid == 0) {
+    ABs[0] = A;
+    ABs[1] = B;
+    ABs[2] = steps;
+    lb_par[0] = __double2float_rd(__dmul_rd(A, 1.0 - e));
+    lb_par[1] = __double2float_ru(__dmul_ru(B, 1.0 + e));
+    lb_par[2] = __double2float_rd(__ddiv_rd(1.0, A));
+    lb_par[3] = __double2float_rd(B);
+    if (out_of_range || A < 1e-6 || A > 1e6 || B > 64.0 * scale_hint) flags[0] = 1;
+  }
+}
+
 static int validate(const gp_assign_args* a) {
   GP_REQUIRE(a != nullptr, "null args");
   GP_REQUIRE(a->d == 2 || a->d == 3, "d must be 2 or 3");
@@ -832,7 +931,7 @@ static int validate(const gp_assign_args* a) {
   GP_REQUIRE(a->m >= 0 && a->m < (1ll << 31), "m out of range");
   GP_REQUIRE(a->wmode == GP_W_UNIT || a->w != nullptr, "weights missing");
   GP_REQUIRE(a->inv2_lo && a->inv2_hi, "inv2 bounds missing");
-  GP_REQUIRE(a->ub_eval && a->ub_norm, "bound maps missing");
+  GP_REQUIRE(a->ub_eval && a->ub_norm && a->lb_par, "bound maps missing");
   return GP_OK;
 }
 
@@ -904,6 +1003,17 @@ int gp_assign_round(const gp_assign_args* args, void* stream) {
   else if (args->wmode == GP_W_F32) launch_round<GP_W_F32>(args, wshift, L, scan, runs, s);
   else launch_round<GP_W_F64>(args, wshift, L, scan, runs, s);
   return check_launch("assign_round");
+}
+
+int gp_update_maps(const double* old_infl, const double* new_infl, const double* moves, int k,
+                   double* state, double* inv2_lo, double* inv2_hi, float* ub_eval,
+                   float* ub_norm, float* lb_par, int32_t* flags, int reset, double scale_hint,
+                   void* stream) {
+  GP_REQUIRE(k >= 1 && old_infl && new_infl && state, "gp_update_maps: bad args");
+  update_maps_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
+      old_infl, new_infl, moves, k, state, inv2_lo, inv2_hi, (float4*)ub_eval, (float4*)ub_norm,
+      lb_par, flags, reset, scale_hint);
+  return check_launch("update_maps");
 }
 
 int gp_rebase_bounds(const gp_assign_args* args, void* stream) {

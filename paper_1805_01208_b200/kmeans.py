@@ -213,7 +213,7 @@ class DevicePartitioner:
             pts = points.to(device=dev, dtype=torch.float64)
         else:
             pts = torch.from_numpy(np.ascontiguousarray(np.asarray(points, dtype=np.float64)))
-            pts = pts.to(dev)
+            pts = pts.to(dev, non_blocking=True)  # DMA straight from pinned callers' buffers
         if pts.dim() != 2:
             raise GeometryError("points must be an (n, d) array")
         w = None
@@ -319,10 +319,18 @@ class DevicePartitioner:
         # (ub~, lb~) float32 pairs: ub~ = +inf (unassigned), lb~ = 0 (kmeans.py:146-147)
         self.UBLB = torch.zeros((n, 2), dtype=torch.float32, device=dev)
         self.UBLB[:, 0] = math.inf
-        # infl | inv2_lo | inv2_hi (float64) and ub_eval | ub_norm (float32, k x 4 each)
-        self.kstate = torch.empty(3 * k, dtype=torch.float64, device=dev)
-        self.kmaps = torch.empty(8 * k, dtype=torch.float32, device=dev)
+        # influences (ping-pong) | inv2_lo | inv2_hi | moves   (float64)
+        self.kstate = torch.empty(5 * k, dtype=torch.float64, device=dev)
+        # device bound maps S[k] | T[k] | A | B | steps, and their float32 parameters
+        self.mapstate = torch.empty(2 * k + 3, dtype=torch.float64, device=dev)
+        self.kmaps = torch.empty(8 * k + 4, dtype=torch.float32, device=dev)
+        self.mapflag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.red = torch.zeros(k + 3, dtype=torch.int64, device=dev)      # block_w | counters
+        # pinned staging for the per-round k-sized transfers
+        self.red_h = torch.empty(k + 3, dtype=torch.int64, pin_memory=True)
+        self.infl_h = torch.empty(k, dtype=torch.float64, pin_memory=True)
+        self.moves_h = torch.empty(k, dtype=torch.float64, pin_memory=True)
+        self.cur = 0
         self.audit_out = torch.zeros(3, dtype=torch.int64, device=dev)
         self.fold_out = torch.empty(k * (d + 3), dtype=torch.float64, device=dev)
         fwb = N.size_query("gp_fold_workspace_bytes", n, 0, n, k)
@@ -335,9 +343,9 @@ class DevicePartitioner:
         a.a, a.ublb = self.A.data_ptr(), self.UBLB.data_ptr()
         a.centers = self.centers_d.data_ptr()
         base = self.kstate.data_ptr()
-        a.infl, a.inv2_lo, a.inv2_hi = base, base + 8 * k, base + 16 * k
+        a.infl, a.inv2_lo, a.inv2_hi = base, base + 16 * k, base + 24 * k
         mb = self.kmaps.data_ptr()
-        a.ub_eval, a.ub_norm = mb, mb + 16 * k
+        a.ub_eval, a.ub_norm, a.lb_par = mb, mb + 16 * k, mb + 32 * k
         a.block_w = self.red.data_ptr()
         a.counters = self.red.data_ptr() + 8 * k
         awb = N.size_query("gp_assign_workspace_bytes", n)
@@ -356,19 +364,29 @@ class DevicePartitioner:
         f.workspace, f.workspace_bytes = self.fold_ws.data_ptr(), self.fold_ws.numel()
         self.fargs = f
 
-    def _push_kstate(self, infl, maps: BoundMaps):
+    def _infl_ptr(self, which):
+        return self.kstate.data_ptr() + 8 * self.settings.k * which
+
+    def _set_influence(self, new_infl, moves=None, reset=False):
+        """Upload the next influences (pinned, async) and compose the bound maps on the
+        device (gp_update_maps): the relaxation of kmeans.py:208-239, lazily."""
         k = self.settings.k
-        inv2 = 1.0 / (infl * infl)
-        inv2_lo = np.nextafter(np.nextafter(inv2, 0.0), 0.0)   # 2 ulps cover the 2 roundings
-        inv2_hi = np.nextafter(np.nextafter(inv2, np.inf), np.inf)
-        host = np.concatenate([infl, inv2_lo, inv2_hi])
-        self.aargs.inv2_min = float(inv2_lo.min())
-        self.kstate.copy_(torch.from_numpy(host), non_blocking=False)
-        ev, nm, la, lb, linv, lblo = maps.device_params()
-        self.kmaps.copy_(torch.from_numpy(np.concatenate([ev.ravel(), nm.ravel()])))
-        a = self.aargs
-        a.lb_a, a.lb_b, a.lb_inva, a.lb_blo = la, lb, linv, lblo
-        del k
+        nxt = 1 - self.cur
+        self.infl_h.numpy()[:] = new_infl
+        self.kstate[nxt * k:(nxt + 1) * k].copy_(self.infl_h, non_blocking=True)
+        mv = None
+        if moves is not None:
+            self.moves_h.numpy()[:] = moves
+            self.kstate[4 * k:5 * k].copy_(self.moves_h, non_blocking=True)
+            mv = self.kstate.data_ptr() + 32 * k
+        old = self._infl_ptr(nxt if reset else self.cur)
+        mb = self.kmaps.data_ptr()
+        N.call("gp_update_maps", old, self._infl_ptr(nxt), mv, k, self.mapstate.data_ptr(),
+               self.aargs.inv2_lo, self.aargs.inv2_hi, mb, mb + 16 * k, mb + 32 * k,
+               self.mapflag.data_ptr(), 1 if reset else 0, self.scale_hint, self.sh)
+        self.cur = nxt
+        self.aargs.infl = self._infl_ptr(nxt)
+        self.aargs.inv2_min = 1.0 / float(np.max(new_infl)) ** 2 * (1.0 - 1e-15)
 
     def _build_grid(self, centers: np.ndarray):
         """Uniform grid over the point box holding the centers (k-sized host numpy),
@@ -460,13 +478,15 @@ class DevicePartitioner:
         N.check(N.lib.gp_assign_round(C.byref(self.aargs), self.sh), "gp_assign_round")
         if self.timer is not None:
             self.timer.events.append((e0, self.timer.mark(self.stream)))
-        host = self.red.cpu().numpy()
+        self.red_h.copy_(self.red, non_blocking=True)
+        self.stream.synchronize()
+        host = self.red_h.numpy()
         k = self.settings.k
         cnt = host[k:k + 3].copy()
         cnt[1] = self.aargs.m  # every active entry is one decision (kmeans.py:309)
         if self.timer is not None:
             self.timer.rounds.append((int(cnt[1]), int(cnt[1] - cnt[0]), int(cnt[2])))
-        return host[:k], cnt
+        return host[:k].copy(), cnt
 
     def _block_weights(self, blk_int):
         if self.wplan.exact:
@@ -486,8 +506,8 @@ class DevicePartitioner:
         infl = np.ones(k)
         block_w = np.zeros(k)
         last_move = np.zeros(k)
-        maps = BoundMaps(k)
-        self._push_kstate(infl, maps)
+        self.scale_hint = max(self.box.diagonal(), 1e-300)
+        self._set_influence(infl, reset=True)
         self._build_grid(centers)
         threshold = st.delta_threshold
         if threshold is None:
@@ -496,7 +516,6 @@ class DevicePartitioner:
         plan = [("sample", s) for s in self.sizes] + [("full", None)] * st.max_iter
         info = None
         fallback = None
-        scale_hint = max(self.box.diagonal(), 1e-300)
         for step, (phase, size) in enumerate(plan):
             m = self._set_active(size)
             # ---------------- assign_and_balance (kmeans.py:377-453)
@@ -531,9 +550,8 @@ class DevicePartitioner:
                 if not target > 0:
                     raise ValueError("target weight must be positive")
                 new_infl = infl * influence_factor(block_w, target, cap, d)
-                maps.relax(infl, new_infl, np.zeros(k))
                 infl = new_infl
-                self._push_kstate(infl, maps)
+                self._set_influence(infl)
             info = BalanceInfo(rounds, final_imb, block_w, skips, decisions, evals, history)
             self._leave_dense()
             if phase == "full" and info.imbalance <= st.epsilon:
@@ -574,22 +592,23 @@ class DevicePartitioner:
                 beta = float(2.0 * extents[nonempty].mean()) if nonempty.any() else 0.0
                 if beta > 0:
                     nxt = eroded(nxt, moves, beta)
-            maps.relax(old_infl, nxt, moves)
             centers = new_centers
             infl = nxt
             last_move = moves
             self.centers_d.copy_(torch.from_numpy(np.ascontiguousarray(centers)))
             self._build_grid(centers)
-            if maps.needs_rebase(scale_hint / max(float(infl.min()), 1e-300)):
-                self._push_kstate(infl, maps)
+            self._set_influence(infl, moves=moves)
+            if int(self.mapflag.item()):
+                # cumulative maps drifted out of range: materialise every bound and restart
+                # from identity maps (result-invariant; only skip tightness changes)
                 a = self.aargs
                 lst, mm = a.list, a.m
                 a.list, a.m = None, n
                 N.count("gp_rebase_bounds")
                 N.check(N.lib.gp_rebase_bounds(C.byref(a), self.sh), "gp_rebase_bounds")
                 a.list, a.m = lst, mm
-                maps.reset()
-            self._push_kstate(infl, maps)
+                self.mapflag.zero_()
+                self._set_influence(infl, reset=True)
 
         final_state = ClusterState(centers, infl, block_w, last_move)
         final_imb = info.imbalance
@@ -626,7 +645,11 @@ def partition_device(points, weights, settings: KMeansSettings, device=None, tim
 
 
 def _finish(assign_dev, stats, k, return_stats):
-    assignment = assign_dev.cpu().numpy()
+    # int64 result (kmeans.py:637-641) into page-locked memory: one DMA, and the
+    # numpy array keeps the pinned tensor alive
+    host = torch.empty(assign_dev.shape, dtype=torch.int64, pin_memory=True)
+    host.copy_(assign_dev)
+    assignment = host.numpy()
     part = Partition(assignment=assignment, k=k, balance_failed=stats.balance_failed,
                      empty_blocks=np.flatnonzero(stats.final_state.block_weights == 0))
     return (part, stats) if return_stats else part
