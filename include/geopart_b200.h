@@ -250,6 +250,20 @@ typedef struct gp_fold_args {
 int gp_fold_workspace_bytes(int64_t n_local, int64_t pos0, int64_t n_global, int k,
                             size_t* bytes);
 int gp_movement_fold(const gp_fold_args* args, void* stream);
+/* Multi-GPU movement reduction.  After gp_movement_fold on a shard,
+ * gp_fold_export writes the shard's (segment, block) partials: keys[p] =
+ * global_segment * k + block, vals[p*6 .. p*6+6) = (w*x_0..w*x_{d-1}, w, objective
+ * padded to 5 columns, extent) and *npairs (device int64).  Every rank then
+ * gathers all ranks' partials and gp_fold_combine folds them per block in global
+ * segment order (the same sequential order as one shard), writing sums / wsum /
+ * extent / objective like gp_movement_fold.  workspace: gp_fold_combine_bytes. */
+int gp_fold_export(const gp_fold_args* args, int64_t* keys, double* vals, int64_t* npairs,
+                   void* stream);
+int gp_fold_combine_bytes(int k, size_t* bytes);
+int gp_fold_combine(const int64_t* keys, const double* vals, int64_t npairs, int k, int d,
+                    int weights_only, double* sums, double* wsum, double* extent,
+                    double* objective, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Debugging aid (synchronises the device): out[4] = {runs, work cursor, valid runs,
  * pairs} of the last gp_movement_fold call. */
 int gp_fold_stats(int64_t* out);

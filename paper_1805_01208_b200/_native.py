@@ -75,6 +75,10 @@ _SIGS = {
     "gp_fold_workspace_bytes": (C.c_int, [i64, i64, i64, C.c_int, C.POINTER(sz)]),
     "gp_movement_fold": (C.c_int, [C.POINTER(FoldArgs), vp]),
     "gp_fold_stats": (C.c_int, [vp]),
+    "gp_fold_export": (C.c_int, [C.POINTER(FoldArgs), vp, vp, vp, vp]),
+    "gp_fold_combine_bytes": (C.c_int, [C.c_int, C.POINTER(sz)]),
+    "gp_fold_combine": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, sz,
+                                  vp]),
     "gp_scatter_by_gid": (C.c_int, [vp, vp, i64, vp, vp]),
     "gp_gather_state": (C.c_int, [vp, i64, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp,
                                   vp]),
@@ -118,7 +122,7 @@ KERNELS_PER_CALL = {
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 3,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 16,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
-    "gp_group_candidates": 1, "gp_sample_ranks": 90, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 1,
+    "gp_group_candidates": 1, "gp_sample_ranks": 90, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
 }
 _launches = [0]
 

@@ -34,7 +34,7 @@ constexpr int FB = 4;       // chunks of 32 positions prefetched per batch
 struct FoldLayout {
   int64_t s0, nseg, cells, cap, pcap;
   size_t off_flags, off_starts, off_rkey, off_skey, off_sidx, off_ridx, off_pbeg, off_slot,
-      off_out, off_counters, off_cub, cub_bytes, off_rpre, off_spos, total;
+      off_out, off_counters, off_cub, cub_bytes, off_rpre, off_spos, off_skey_final, total;
 };
 
 static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k) {
@@ -63,6 +63,7 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   L.off_starts = o; o = al(o + (L.cap + 1) * 4);
   L.off_rkey = o; o = al(o + L.cap * 4);
   L.off_skey = o; o = al(o + L.cap * 4);
+  L.off_skey_final = L.off_skey;
   L.off_sidx = o; o = al(o + L.cap * 4);
   L.off_ridx = o; o = al(o + L.cap * 4);
   L.off_pbeg = o; o = al(o + (L.pcap + 1) * 4);
@@ -317,6 +318,31 @@ __global__ void fold_combine(gp_fold_args f, const int32_t* __restrict__ slot, i
   }
 }
 
+__global__ void fold_export_kernel(const uint32_t* __restrict__ skey,
+                                   const int32_t* __restrict__ pbeg,
+                                   const int64_t* __restrict__ counters,
+                                   const double* __restrict__ out, int64_t s0, int k,
+                                   int64_t* __restrict__ keys, double* __restrict__ vals,
+                                   int64_t* npairs) {
+  const int64_t P = counters[3];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *npairs = P;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = skey[pbeg[p]];
+    const int64_t seg = key / (uint32_t)k + s0, c = key % (uint32_t)k;
+    keys[p] = seg * k + c;
+#pragma unroll
+    for (int j = 0; j < MAXCOL + 1; ++j) vals[p * (MAXCOL + 1) + j] = out[p * (MAXCOL + 1) + j];
+  }
+}
+
+__global__ void combine_slots(const int64_t* __restrict__ keys, int64_t npairs,
+                              int32_t* __restrict__ slot) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
+       p += (int64_t)gridDim.x * blockDim.x)
+    slot[keys[p]] = (int32_t)p;
+}
+
 }  // namespace gp
 
 using namespace gp;
@@ -331,6 +357,48 @@ int gp_fold_stats(int64_t* out) {
   GP_CUDA(cudaDeviceSynchronize());
   GP_CUDA(cudaMemcpy(out, g_last_counters, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost));
   return GP_OK;
+}
+
+int gp_fold_export(const gp_fold_args* f, int64_t* keys, double* vals, int64_t* npairs,
+                   void* stream) {
+  GP_REQUIRE(f && keys && vals && npairs, "gp_fold_export: bad args");
+  FoldLayout L = layout(f->n_local, f->pos0, f->n_global, f->k);
+  char* ws = (char*)f->workspace;
+  fold_export_kernel<<<grid_for(L.pcap, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+      (const uint32_t*)(ws + L.off_skey_final), (const int32_t*)(ws + L.off_pbeg),
+      (const int64_t*)(ws + L.off_counters), (const double*)(ws + L.off_out), L.s0, f->k, keys,
+      vals, npairs);
+  return check_launch("fold_export");
+}
+
+int gp_fold_combine_bytes(int k, size_t* bytes) {
+  GP_REQUIRE(k >= 1, "gp_fold_combine_bytes: bad k");
+  *bytes = (size_t)GP_SEGMENTS * k * sizeof(int32_t);
+  return GP_OK;
+}
+
+int gp_fold_combine(const int64_t* keys, const double* vals, int64_t npairs, int k, int d,
+                    int weights_only, double* sums, double* wsum, double* extent,
+                    double* objective, void* workspace, size_t workspace_bytes, void* stream) {
+  GP_REQUIRE(d == 2 || d == 3, "gp_fold_combine: bad d");
+  GP_REQUIRE(workspace_bytes >= (size_t)GP_SEGMENTS * k * sizeof(int32_t),
+             "gp_fold_combine: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* slot = (int32_t*)workspace;
+  GP_CUDA(cudaMemsetAsync(slot, 0xff, (size_t)GP_SEGMENTS * k * sizeof(int32_t), s));
+  if (npairs > 0)
+    combine_slots<<<grid_for(npairs, 256, 148 * 8), 256, 0, s>>>(keys, npairs, slot);
+  gp_fold_args f{};
+  f.d = d;
+  f.k = k;
+  f.weights_only = weights_only;
+  f.sums = sums;
+  f.wsum = wsum;
+  f.extent = extent;
+  f.objective = objective;
+  if (d == 2) fold_combine<2><<<grid_for(k, 4), 128, 0, s>>>(f, slot, GP_SEGMENTS, vals);
+  else fold_combine<3><<<grid_for(k, 4), 128, 0, s>>>(f, slot, GP_SEGMENTS, vals);
+  return check_launch("fold_combine");
 }
 
 int gp_fold_workspace_bytes(int64_t n_local, int64_t pos0, int64_t n_global, int k,
@@ -392,6 +460,12 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     GP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, b, kb, vb, (int)R, 0, 32, s));
     skey = kb.Current();
     sidx = vb.Current();
+    if (skey != (uint32_t*)(ws + L.off_skey_final)) {
+      // keep the sorted keys where gp_fold_export expects them
+      GP_CUDA(cudaMemcpyAsync(ws + L.off_skey_final, skey, R * sizeof(uint32_t),
+                              cudaMemcpyDeviceToDevice, s));
+      skey = (uint32_t*)(ws + L.off_skey_final);
+    }
     fold_pair_flags<<<grid_for(R, 256, sms * 16), 256, 0, s>>>(skey, R, counters, flags);
     b = L.cub_bytes;
     GP_CUDA(cub::DeviceSelect::Flagged(cub_tmp, b, cub::CountingInputIterator<int32_t>(0), flags,

@@ -244,6 +244,7 @@ class DevicePartitioner:
         pts, w = self._input(points, weights)
         n, d = pts.shape
         self.n, self.d = n, d
+        self.n_global, self.pos0 = n, 0
         k = st.k
         if k > n:
             raise ValueError(f"k={k} exceeds the number of points {n}")
@@ -333,7 +334,7 @@ class DevicePartitioner:
         self.cur = 0
         self.audit_out = torch.zeros(3, dtype=torch.int64, device=dev)
         self.fold_out = torch.empty(k * (d + 3), dtype=torch.float64, device=dev)
-        fwb = N.size_query("gp_fold_workspace_bytes", n, 0, n, k)
+        fwb = N.size_query("gp_fold_workspace_bytes", n, self.pos0, self.n_global, k)
         self.fold_ws = torch.empty(max(fwb, 8), dtype=torch.uint8, device=dev)
         a = N.AssignArgs()
         a.X, a.ldx, a.d, a.k, a.order3 = self.X.data_ptr(), self.ldx, d, k, self.order3
@@ -356,7 +357,7 @@ class DevicePartitioner:
         f = N.FoldArgs()
         f.X, f.ldx, f.d, f.k, f.order3 = self.X.data_ptr(), self.ldx, d, k, self.order3
         f.wmode, f.w, f.a = a.wmode, a.w, self.A.data_ptr()
-        f.n_local, f.pos0, f.n_global = n, 0, n
+        f.n_local, f.pos0, f.n_global = n, self.pos0, self.n_global
         f.centers = self.centers_d.data_ptr()
         fo = self.fold_out.data_ptr()
         f.sums, f.wsum, f.extent, f.objective = fo, fo + 8 * k * d, fo + 8 * k * (d + 1), \
@@ -478,23 +479,37 @@ class DevicePartitioner:
         N.check(N.lib.gp_assign_round(C.byref(self.aargs), self.sh), "gp_assign_round")
         if self.timer is not None:
             self.timer.events.append((e0, self.timer.mark(self.stream)))
+        self._reduce_round()
         self.red_h.copy_(self.red, non_blocking=True)
         self.stream.synchronize()
         host = self.red_h.numpy()
         k = self.settings.k
         cnt = host[k:k + 3].copy()
-        cnt[1] = self.aargs.m  # every active entry is one decision (kmeans.py:309)
+        cnt[1] = self.m_global  # every active entry is one decision (kmeans.py:309)
         if self.timer is not None:
             self.timer.rounds.append((int(cnt[1]), int(cnt[1] - cnt[0]), int(cnt[2])))
         return host[:k].copy(), cnt
 
+    # ---- hooks the multi-GPU partitioner overrides (one shard: nothing to exchange)
+    def _reduce_round(self):
+        pass
+
+    def _audit_totals(self):
+        return self.audit_out.cpu().numpy()
+
+    def _global_count(self, m):
+        return m
+
+    def _fold(self, weights_only):
+        f = self.fargs
+        f.weights_only = weights_only
+        N.count("gp_movement_fold")
+        N.check(N.lib.gp_movement_fold(C.byref(f), self.sh), "gp_movement_fold")
+
     def _block_weights(self, blk_int):
         if self.wplan.exact:
             return blk_int.astype(np.float64) / self.wplan.scale
-        f = self.fargs
-        f.weights_only = 1
-        N.count("gp_movement_fold")
-        N.check(N.lib.gp_movement_fold(C.byref(f), self.sh), "gp_movement_fold")
+        self._fold(1)
         k = self.settings.k
         return self.fold_out[k * self.d:k * (self.d + 1)].cpu().numpy().copy()
 
@@ -518,6 +533,7 @@ class DevicePartitioner:
         fallback = None
         for step, (phase, size) in enumerate(plan):
             m = self._set_active(size)
+            self.m_global = self._global_count(m)
             # ---------------- assign_and_balance (kmeans.py:377-453)
             skips = decisions = evals = 0
             final_imb = math.inf
@@ -561,10 +577,7 @@ class DevicePartitioner:
                 fallback = (ClusterState(centers.copy(), infl.copy(), block_w.copy(),
                                          last_move.copy()), info.imbalance)
             # ---------------- movement (kmeans.py:585-626)
-            f = self.fargs
-            f.weights_only = 0
-            N.count("gp_movement_fold")
-            N.check(N.lib.gp_movement_fold(C.byref(f), self.sh), "gp_movement_fold")
+            self._fold(0)
             red = self.fold_out.cpu().numpy()
             sums = red[:k * d].reshape(k, d)
             totals = red[k * d:k * (d + 1)]
@@ -576,7 +589,7 @@ class DevicePartitioner:
             new_centers[empty] = centers[empty]
             moves = np.linalg.norm(new_centers - centers, axis=1)
             stats.iterations.append(IterationRecord(
-                phase=phase, active_points=m, balance_rounds=info.rounds,
+                phase=phase, active_points=self.m_global, balance_rounds=info.rounds,
                 imbalance=info.imbalance, skip_decisions=info.skip_decisions,
                 total_decisions=info.total_decisions, distance_evals=info.distance_evals,
                 objective=float(obj_parts.sum()), max_move=float(moves.max())))
@@ -619,14 +632,20 @@ class DevicePartitioner:
         stats.balance_failed = final_imb > st.epsilon
         stats.final_state = final_state
         if st.audit_bounds:
-            aud = self.audit_out.cpu().numpy()
+            aud = self._audit_totals()
             stats.audited_point_iterations = int(aud[0])
             stats.bound_violations = int(aud[1])
             stats.skip_check_failures = int(aud[2])
-        out = torch.empty(n, dtype=torch.int64, device=self.device)
-        N.call("gp_scatter_by_gid", A.data_ptr(), self.gids.data_ptr(), n, out.data_ptr(), self.sh)
+        out = self._deliver(A)
         self.release()
         return out, stats
+
+    def _deliver(self, A):
+        """int64 assignment by original id (kmeans.py:637-641)."""
+        out = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        N.call("gp_scatter_by_gid", A.data_ptr(), self.gids.data_ptr(), self.n, out.data_ptr(),
+               self.sh)
+        return out
 
     def release(self):
         """Drop every n-sized device buffer (the caller keeps only the result)."""
@@ -635,6 +654,219 @@ class DevicePartitioner:
                      "grid_items"):
             if hasattr(self, name):
                 setattr(self, name, None)
+
+
+class DistributedPartitioner(DevicePartitioner):
+    """One shard of a multi-GPU partition (one process per GPU, torch.distributed).
+
+    Every rank passes its own contiguous block of the original rows (in rank order,
+    like RankWorld.from_points deals them).  The SFC bootstrap redistributes points into
+    contiguous ranges of the global (key, gid) order on 256-segment boundaries
+    (parallel.sfc_redistribute); each balance round all-reduces the k exact int64 block
+    weights; each movement iteration gathers the (segment, block) fold partials and folds
+    them in global segment order.  All k-sized host math is identical on every rank, so
+    the result is bit-identical to one GPU's (and to the reference's).
+    """
+
+    def __init__(self, settings, comm, device=None, timer=None):
+        super().__init__(settings, device=device, timer=timer)
+        self.comm = comm
+
+    # ---------------------------------------------------------------- bootstrap
+    def _device_sort(self, keys: torch.Tensor) -> torch.Tensor:
+        """Stable permutation sorting int64 keys (device radix sort, gp_sort_pairs)."""
+        m = keys.shape[0]
+        vals = torch.arange(m, dtype=torch.int32, device=keys.device)
+        ko = torch.empty_like(keys)
+        vo = torch.empty_like(vals)
+        wsb = N.size_query("gp_sort_workspace_bytes", m)
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=keys.device)
+        N.call("gp_sort_pairs", keys.data_ptr(), vals.data_ptr(), ko.data_ptr(), vo.data_ptr(), m,
+               self.key_bits, ws.data_ptr(), wsb, self.sh)
+        return vo.long()
+
+    def bootstrap(self, points, weights):
+        from . import parallel as P
+
+        st, comm = self.settings, self.comm
+        pts, w = self._input(points, weights)
+        n_in, d = pts.shape
+        self.d = d
+        off, n = P.input_offsets(n_in, comm)
+        self.in_offset, self.n_in = off, n_in
+        k = st.k
+        if k > n:
+            raise ValueError(f"k={k} exceeds the number of points {n}")
+        depth = st.sfc_depth if st.sfc_depth is not None else DEFAULT_DEPTH.get(d)
+        if depth is None or d not in (2, 3):
+            raise GeometryError(f"unsupported dimension {d}")
+        if d * depth > 62:
+            raise GeometryError(f"depth {depth} out of range for dimension {d}")
+        if n_in < 1:
+            raise ValueError("every rank needs at least one point")
+        self.key_bits = d * depth
+        dev, sh = self.device, self.sh
+        sp, sd = pts.stride()
+        # K1 box: local min/max + allreduce MIN/MAX (kmeans.py:546-548)
+        lohi = torch.empty(2 * d, dtype=torch.float64, device=dev)
+        bad = torch.empty(1, dtype=torch.int32, device=dev)
+        N.call("gp_box_minmax", pts.data_ptr(), n_in, d, sp, sd, lohi.data_ptr(), bad.data_ptr(), sh)
+        comm.allreduce(lohi[:d], P.dist.ReduceOp.MIN)
+        comm.allreduce(lohi[d:], P.dist.ReduceOp.MAX)
+        comm.allreduce(bad, P.dist.ReduceOp.MAX)
+        lohi_h = lohi.cpu().numpy()
+        if int(bad.item()):
+            raise GeometryError("non-finite box corner")
+        self.box = BoundingBox(lohi_h[:d].copy(), lohi_h[d:].copy())
+        # weight plan agreed by all ranks
+        self.wplan = self._weight_plan_global(w, n_in, n)
+        # K2 keys (gids = global ids) + local sort
+        keys = torch.empty(n_in, dtype=torch.int64, device=dev)
+        gids = torch.empty(n_in, dtype=torch.int32, device=dev)
+        N.call("gp_hilbert_keys", pts.data_ptr(), n_in, d, sp, sd, lohi.data_ptr(), depth,
+               keys.data_ptr(), gids.data_ptr(), off, sh)
+        perm = self._device_sort(keys)
+        keys_s = keys[perm]
+        gids_s = gids[perm]
+        local_idx = (gids_s - off).to(torch.int32)
+        X_s = torch.empty((n_in, d), dtype=torch.float64, device=dev)
+        W_s = None
+        if w is not None:
+            W_s = torch.empty(n_in, dtype=torch.float32 if self.wplan.mode == 1 else torch.float64,
+                              device=dev)
+        N.call("gp_gather_points", pts.data_ptr(), sp, sd, d, local_idx.data_ptr(), n_in,
+               X_s.data_ptr(), d, _ptr(w), self.wplan.mode if w is not None else 0, _ptr(W_s), sh)
+        payload = [gids_s, X_s] + ([W_s] if W_s is not None else [])
+        keys_r, pay_r = P.sfc_redistribute(keys_s, payload, n, comm, self.key_bits,
+                                           self._device_sort)
+        del keys, gids, perm, keys_s, gids_s, local_idx, X_s, W_s, payload
+        bounds = P.shard_bounds(n, comm.world)
+        self.n, self.pos0, self.n_global = int(keys_r.shape[0]), int(bounds[comm.rank]), n
+        assert self.n == bounds[comm.rank + 1] - bounds[comm.rank]
+        self.gids = pay_r[0].contiguous()
+        self.X = pay_r[1].contiguous()
+        self.W = pay_r[2].contiguous() if w is not None else None
+        self.ldx = d
+        self.keys_sorted = keys_r if self.keep_keys else None
+        # K4 initial centers: the owner of each global position contributes its rows
+        pos = initial_center_positions(n, k)
+        mine = pos[(pos >= self.pos0) & (pos < self.pos0 + self.n)] - self.pos0
+        rows = self.X[torch.from_numpy(mine).to(dev)] if len(mine) else \
+            torch.empty((0, d), dtype=torch.float64, device=dev)
+        cen = torch.cat(comm.allgather_var(rows)).contiguous()
+        self.centers_d = cen
+        self.init_centers = cen.cpu().numpy().copy()
+        # warm-up sample order over all n (every rank derives the same permutation)
+        self.sizes = sample_schedule(n, st.init_sample)
+        if self.sizes:
+            rank_d = sample_ranks_device(n, st.seed, dev, sh)
+            self.rank_sfc = torch.empty(self.n, dtype=torch.int32, device=dev)
+            N.call("gp_gather_ranks", rank_d.data_ptr(), self.gids.data_ptr(), self.n,
+                   self.rank_sfc.data_ptr(), sh)
+            cwb = N.size_query("gp_compact_workspace_bytes", self.n)
+            self.compact_ws = torch.empty(max(cwb, 8), dtype=torch.uint8, device=dev)
+            self.active_idx = torch.empty(self.n, dtype=torch.int32, device=dev)
+            self.active_cnt = torch.empty(1, dtype=torch.int64, device=dev)
+            del rank_d
+        del pts, w
+        return self
+
+    def _weight_plan_global(self, w, n_in, n) -> _WeightPlan:
+        from . import parallel as P
+
+        flags = torch.zeros(4, dtype=torch.float64, device=self.device)
+        has = torch.tensor([0.0 if w is None else 1.0], dtype=torch.float64, device=self.device)
+        self.comm.allreduce(has, P.dist.ReduceOp.MAX)
+        if float(has.item()) == 0.0:
+            return _WeightPlan(0, True, 1.0)
+        if w is None:
+            raise ValueError("weights must be given on every rank or on none")
+        out = torch.empty(3, dtype=torch.int64, device=self.device)
+        N.call("gp_weight_probe", w.data_ptr(), n_in, out.data_ptr(), self.sh)
+        fl, low, mxb = (int(v) for v in out.cpu().tolist())
+        mx = float(np.array([mxb], dtype=np.int64).view(np.float64)[0])
+        flags[0] = float(fl & 1)
+        flags[1] = float((fl >> 1) & 1)
+        flags[2] = float(-low)
+        flags[3] = mx
+        self.comm.allreduce(flags, P.dist.ReduceOp.MAX)
+        f = flags.cpu().numpy()
+        if f[0]:
+            return _WeightPlan(2, False, 1.0)
+        mode = 2 if f[1] else 1
+        low = -int(f[2])
+        s = max(0, -low) if low < 4096 else 0
+        exact = s <= 1000 and f[3] * 2.0 ** s * n < 2.0 ** 53
+        return _WeightPlan(mode, bool(exact), 2.0 ** s if exact else 1.0)
+
+    # ---------------------------------------------------------------- exchanges
+    def _reduce_round(self):
+        self.comm.allreduce(self.red)
+
+    def _global_count(self, m):
+        t = torch.tensor([m], dtype=torch.int64, device=self.device)
+        return int(self.comm.allreduce(t).item())
+
+    def _audit_totals(self):
+        return self.comm.allreduce(self.audit_out.clone()).cpu().numpy()
+
+    def _fold(self, weights_only):
+        from . import parallel as P
+
+        super()._fold(weights_only)
+        k, d = self.settings.k, self.d
+        if not hasattr(self, "pair_keys"):
+            cap = min((256 // self.comm.world + 2) * k, self.n + 1)
+            self.pair_keys = torch.empty(cap, dtype=torch.int64, device=self.device)
+            self.pair_vals = torch.empty((cap, 6), dtype=torch.float64, device=self.device)
+            self.pair_n = torch.empty(1, dtype=torch.int64, device=self.device)
+            cb = N.size_query("gp_fold_combine_bytes", k)
+            self.combine_ws = torch.empty(cb, dtype=torch.uint8, device=self.device)
+        N.call("gp_fold_export", C.byref(self.fargs), self.pair_keys.data_ptr(),
+               self.pair_vals.data_ptr(), self.pair_n.data_ptr(), self.sh)
+        npairs = int(self.pair_n.item())
+        keys, vals = P.gather_fold_pairs(self.pair_keys[:npairs], self.pair_vals[:npairs],
+                                         self.comm)
+        keys, vals = keys.contiguous(), vals.contiguous()
+        fo = self.fold_out.data_ptr()
+        N.call("gp_fold_combine", keys.data_ptr(), vals.data_ptr(), keys.shape[0], k, d,
+               weights_only, fo, fo + 8 * k * d, fo + 8 * k * (d + 1), fo + 8 * k * (d + 2),
+               self.combine_ws.data_ptr(), self.combine_ws.numel(), self.sh)
+
+    def _deliver(self, A):
+        """Labels of this rank's own input rows, routed back from the SFC shards."""
+        from . import parallel as P
+
+        comm = self.comm
+        offs = torch.tensor([t.item() for t in comm.allgather_var(
+            torch.tensor([self.in_offset], dtype=torch.int64, device=self.device))] + [
+            self.n_global], dtype=torch.int64, device=self.device)
+        g = self.gids.long()
+        owner = torch.searchsorted(offs, g, right=True) - 1
+        order = torch.sort(owner, stable=True).indices
+        send = torch.bincount(owner, minlength=comm.world).tolist()
+        pair = torch.stack([g[order], A.long()[order]], dim=1)
+        recv, _ = comm.alltoall(pair, send)
+        out = torch.empty(self.n_in, dtype=torch.int64, device=self.device)
+        out[recv[:, 0] - self.in_offset] = recv[:, 1]
+        return out
+
+    def release(self):
+        super().release()
+        for name in ("pair_keys", "pair_vals", "combine_ws"):
+            if hasattr(self, name):
+                setattr(self, name, None)
+
+
+def partition_distributed(points, weights, settings: KMeansSettings, group=None, device=None,
+                          timer=None):
+    """Multi-GPU partition: this rank's contiguous block of original rows in, their
+    int64 labels (device tensor) and the (global, rank-identical) KMeansStats out."""
+    from .parallel import Comm
+
+    eng = DistributedPartitioner(settings, Comm(group), device=device, timer=timer)
+    eng.bootstrap(points, weights)
+    return eng.run()
 
 
 def partition_device(points, weights, settings: KMeansSettings, device=None, timer=None):
