@@ -233,12 +233,18 @@ def run_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("GP_DIST_BACKEND", "nccl") != "nccl":
+        local = 0  # test mode: every rank shares GPU 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("GP_DIST_BACKEND", "nccl")  # gloo: several ranks on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     c, pts_d, w_d, host_inputs = device_workload(args.config, dev)
     n, d = pts_d.shape
