@@ -175,6 +175,12 @@ typedef struct gp_assign_args {
   double grid_lo[3];
   double grid_h;
   double inv2_min;        /* lower bound of min_c 1/infl_c^2 */
+  /* static box of every scan unit (gp_group_boxes over the active entries with
+   * shift = unit_shift = log2(scan_regions * 256)); NULL: boxes of the scanned
+   * points are computed per round */
+  const double* unit_boxes;
+  int32_t unit_shift;
+  int32_t pad1;
 } gp_assign_args;
 int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);

@@ -33,7 +33,7 @@ class AssignArgs(C.Structure):
         ("group_list", vp), ("group_count", vp), ("group_cap", i32), ("group_shift", i32),
         ("workspace", vp), ("workspace_bytes", sz), ("scan_regions", i32), ("grid_n", i32),
         ("grid_start", vp), ("grid_items", vp), ("grid_lo", f64 * 3), ("grid_h", f64),
-        ("inv2_min", f64),
+        ("inv2_min", f64), ("unit_boxes", vp), ("unit_shift", i32), ("pad1", i32),
     ]
 
 

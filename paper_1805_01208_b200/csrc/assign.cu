@@ -103,7 +103,7 @@ constexpr int FCHUNK = FTH * FPER;    // entries per CTA chunk (2048 = 8 regions
 
 struct AssignLayout {
   int64_t nchunks, nregions;
-  size_t off_list, off_runs, total;
+  size_t off_list, off_olda, off_runs, total;
 };
 
 static AssignLayout assign_layout(int64_t m) {
@@ -114,6 +114,7 @@ static AssignLayout assign_layout(int64_t m) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   size_t o = 0;
   L.off_list = o; o = al(o + (size_t)L.nregions * WREG * 4);
+  L.off_olda = o; o = al(o + (size_t)L.nregions * WREG * 4);
   L.off_runs = o; o = al(o + (size_t)L.nregions * 4);
   L.total = o;
   return L;
@@ -127,6 +128,7 @@ static AssignLayout assign_layout(int64_t m) {
 template <int WM>
 __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshift, int64_t nchunks,
                                                      int32_t* __restrict__ scan,
+                                                     int32_t* __restrict__ olda,
                                                      int32_t* __restrict__ runs) {
   __shared__ int s_ckey[HSLOTS];
   __shared__ long long s_cval[HSLOTS];
@@ -175,13 +177,18 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
     int run_a = -1;
     long long run_w = 0;
     bool broke = false;
+    int ea = -1;          // cluster whose bound parameters E holds (runs share them)
+    float4 E = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int e = 0; e < FPER; ++e) {
       if (q[e] < 0) continue;
       bool skip = false;
       const int ae = a[e];
       if (ae >= 0) {
-        const float4 E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
+        if (ae != ea) {
+          E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
+          ea = ae;
+        }
         skip = ub_evalf(E, ub[e]) < lb_evalf(lbp.x, lb[e], lbp.y);
       }
       if (!skip) {
@@ -218,9 +225,14 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
     }
     int off = incl - mine;
     int32_t* dst = scan + reg * WREG;
+    int32_t* dsa = olda + reg * WREG;
 #pragma unroll
     for (int e = 0; e < FPER; ++e)
-      if (need & (1u << e)) dst[off++] = q[e];
+      if (need & (1u << e)) {
+        dst[off] = q[e];
+        dsa[off] = a[e];  // the scan writes a only when the block changes
+        ++off;
+      }
     if (lane == 31) runs[reg] = incl;
   }
   for (int o = 16; o; o >>= 1) nskip += __shfl_xor_sync(FULL, nskip, o);
@@ -388,6 +400,7 @@ __device__ void grid_point(const gp_assign_args& p, const double* x, int& bi, fl
 template <int D, int WM>
 __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
                                                    int sreg, const int32_t* __restrict__ scan,
+                                                   const int32_t* __restrict__ olda,
                                                    const int32_t* __restrict__ runs) {
   __shared__ WarpCand<D> WCs[STH / 32];
   __shared__ int s_ckey[HSLOTS];
@@ -424,7 +437,7 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
 #pragma unroll
     for (int r = 0; r < SREG; ++r) rbeg[r] = __shfl_sync(FULL, incl - cnt_here, r);
     // v-th scanned point of the unit -> position (static register indexing only)
-    auto pos_of = [&](int v) {
+    auto slot_of = [&](int v) {
       int r = 0, rb = 0;
 #pragma unroll
       for (int t = 1; t < SREG; ++t)
@@ -432,8 +445,9 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
           r = t;
           rb = rbeg[t];
         }
-      return scan[(unit * sreg + r) * WREG + (v - rb)];
+      return (unit * sreg + r) * WREG + (v - rb);
     };
+    auto pos_of = [&](int v) { return scan[slot_of(v)]; };
     // candidate source: the group's hierarchical list, or all k centers
     const int32_t* src = nullptr;
     int nsrc = p.k;
@@ -445,30 +459,39 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
         nsrc = gc;
       }
     }
-    // ---- box of the unit's scanned points
+    // ---- box: the unit's static box (all its active entries), or the box of the
+    // unit's scanned points
     double lo[D], hi[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      lo[j] = INFINITY;
-      hi[j] = -INFINITY;
-    }
-    for (int v = lane; v < total_pts; v += 32) {
-      const int q = pos_of(v);
-#pragma unroll
-      double xq[D];
-      load_point<D>(p.X, p.ldx, q, xq);
+    if (p.unit_boxes) {
+      const int64_t u = (unit * sreg * WREG) >> p.unit_shift;
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        lo[j] = fmin(lo[j], xq[j]);
-        hi[j] = fmax(hi[j], xq[j]);
+        lo[j] = p.unit_boxes[u * 2 * D + j];
+        hi[j] = p.unit_boxes[u * 2 * D + D + j];
       }
-    }
+    } else {
 #pragma unroll
-    for (int j = 0; j < D; ++j)
-      for (int o = 16; o; o >>= 1) {
-        lo[j] = fmin(lo[j], __shfl_xor_sync(FULL, lo[j], o));
-        hi[j] = fmax(hi[j], __shfl_xor_sync(FULL, hi[j], o));
+      for (int j = 0; j < D; ++j) {
+        lo[j] = INFINITY;
+        hi[j] = -INFINITY;
       }
+      for (int v = lane; v < total_pts; v += 32) {
+        const int q = pos_of(v);
+        double xq[D];
+        load_point<D>(p.X, p.ldx, q, xq);
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          lo[j] = fmin(lo[j], xq[j]);
+          hi[j] = fmax(hi[j], xq[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        for (int o = 16; o; o >>= 1) {
+          lo[j] = fmin(lo[j], __shfl_xor_sync(FULL, lo[j], o));
+          hi[j] = fmax(hi[j], __shfl_xor_sync(FULL, hi[j], o));
+        }
+    }
     // ---- candidates: lsq <= second smallest usq over the source
     double m1 = INFINITY, m2 = INFINITY;
     for (int i = lane; i < nsrc; i += 32) {
@@ -533,7 +556,7 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
         unsigned long long nn = 0;
         grid_point<D>(p, x, bi, bestf, secondf, nn);
         nq += nn;
-        p.a[q] = bi;
+        if (olda[slot_of(v)] != bi) p.a[q] = bi;
         store_bounds(p, q, bi, bestf, secondf);
         cache_add(s_ckey, s_cval, p.block_w, bi, weight_units<WM>(p.w, q, wshift));
       }
@@ -632,7 +655,7 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
       int c = -1;
       if (valid) {
         c = bi;
-        p.a[q] = c;
+        if (olda[slot_of(v)] != c) p.a[q] = c;   // most rescans keep their block
         store_bounds(p, q, c, bestf, secondf);
         wv = weight_units<WM>(p.w, q, wshift);
       }
@@ -949,9 +972,9 @@ static int g_sreg = 0;  // 0: automatic (GP_SCAN_REGIONS overrides)
 
 template <int WM>
 static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout& L,
-                         int32_t* scan, int32_t* runs, cudaStream_t s) {
+                         int32_t* scan, int32_t* olda, int32_t* runs, cudaStream_t s) {
   unsigned gf = persistent_grid((const void*)filter_kernel<WM>, FTH, L.nchunks);
-  filter_kernel<WM><<<gf, FTH, 0, s>>>(*a, wshift, L.nchunks, scan, runs);
+  filter_kernel<WM><<<gf, FTH, 0, s>>>(*a, wshift, L.nchunks, scan, olda, runs);
   if (g_sreg == 0) {
     const char* e = getenv("GP_SCAN_REGIONS");
     g_sreg = e ? atoi(e) : -1;
@@ -963,10 +986,10 @@ static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout
   const int64_t wgroups = (L.nregions + sreg * (STH / 32) - 1) / (sreg * (STH / 32));
   if (a->d == 2) {
     unsigned gs = persistent_grid((const void*)scan_kernel<2, WM>, STH, wgroups);
-    scan_kernel<2, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, runs);
+    scan_kernel<2, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs);
   } else {
     unsigned gs = persistent_grid((const void*)scan_kernel<3, WM>, STH, wgroups);
-    scan_kernel<3, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, runs);
+    scan_kernel<3, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs);
   }
 }
 
@@ -991,6 +1014,9 @@ int gp_assign_round(const gp_assign_args* args, void* stream) {
              "gp_assign_round: workspace too small");
   if (args->group_list)
     GP_REQUIRE(SREG * WREG <= (1ll << args->group_shift), "group_shift smaller than a scan unit");
+  if (args->unit_boxes)
+    GP_REQUIRE(args->scan_regions >= 1 && (1ll << args->unit_shift) == args->scan_regions * WREG,
+               "unit_shift must equal log2(scan_regions * 256)");
   int wshift = 0;
   frexp(args->wscale, &wshift);
   wshift -= 1;
@@ -998,10 +1024,11 @@ int gp_assign_round(const gp_assign_args* args, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   char* ws = (char*)args->workspace;
   int32_t* scan = (int32_t*)(ws + L.off_list);
+  int32_t* olda = (int32_t*)(ws + L.off_olda);
   int32_t* runs = (int32_t*)(ws + L.off_runs);
-  if (args->wmode == GP_W_UNIT) launch_round<GP_W_UNIT>(args, wshift, L, scan, runs, s);
-  else if (args->wmode == GP_W_F32) launch_round<GP_W_F32>(args, wshift, L, scan, runs, s);
-  else launch_round<GP_W_F64>(args, wshift, L, scan, runs, s);
+  if (args->wmode == GP_W_UNIT) launch_round<GP_W_UNIT>(args, wshift, L, scan, olda, runs, s);
+  else if (args->wmode == GP_W_F32) launch_round<GP_W_F32>(args, wshift, L, scan, olda, runs, s);
+  else launch_round<GP_W_F64>(args, wshift, L, scan, olda, runs, s);
   return check_launch("assign_round");
 }
 

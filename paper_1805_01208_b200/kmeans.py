@@ -420,7 +420,26 @@ class DevicePartitioner:
             self._enter_dense(m)
         if self.hier is not None:
             self.hier.prepare(self.aargs.list, m)
+        self._unit_boxes(m)
         return m
+
+    def _unit_boxes(self, m):
+        """Static box of every scan unit over its active entries (once per active set)."""
+        a = self.aargs
+        shift = 8 + (a.scan_regions.bit_length() - 1)
+        key = (a.X, a.list, m, shift)
+        if getattr(self, "ubox_key", None) == key:   # the full phase's set never changes
+            a.unit_boxes, a.unit_shift = self.ubox.data_ptr(), shift
+            return
+        self.ubox_key = key
+        nu = max(1, (m + (1 << shift) - 1) >> shift)
+        if getattr(self, "ubox_cap", 0) < nu:
+            self.ubox_cap = max(nu, (self.n + 255) >> 8)
+            self.ubox = torch.empty(self.ubox_cap * 2 * self.d, dtype=torch.float64,
+                                    device=self.device)
+        N.call("gp_group_boxes", a.X, self.ldx, self.d, a.list, m, shift, self.ubox.data_ptr(),
+               self.sh)
+        a.unit_boxes, a.unit_shift = self.ubox.data_ptr(), shift
 
     def _enter_dense(self, m):
         """Sample phase: gather the active entries' state into dense arrays so the
@@ -651,7 +670,7 @@ class DevicePartitioner:
         """Drop every n-sized device buffer (the caller keeps only the result)."""
         for name in ("X", "W", "A", "A_fb", "UBLB", "A_d", "UBLB_d", "X_d", "W_d", "gids", "rank_sfc", "active_idx",
                      "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier", "grid_start",
-                     "grid_items"):
+                     "grid_items", "ubox"):
             if hasattr(self, name):
                 setattr(self, name, None)
 
