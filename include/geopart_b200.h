@@ -180,7 +180,7 @@ typedef struct gp_assign_args {
    * points are computed per round */
   const double* unit_boxes;
   int32_t unit_shift;
-  int32_t pad1;
+  int32_t flags;          /* bit 0: accumulate scan statistics (gp_scan_stats) */
 } gp_assign_args;
 int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);
@@ -252,6 +252,11 @@ typedef struct gp_fold_args {
   /* scratch */
   void* workspace;
   size_t workspace_bytes;
+  /* optional dense entry list: when list != NULL the entries are i = 0..m-1 at
+   * local positions list[i] (ascending), and X, w, a are indexed by i (the dense
+   * warm-up sample arrays); NULL: entry i is local position i, i < n_local */
+  const int32_t* list;
+  int64_t m;
 } gp_fold_args;
 int gp_fold_workspace_bytes(int64_t n_local, int64_t pos0, int64_t n_global, int k,
                             size_t* bytes);
@@ -273,6 +278,12 @@ int gp_fold_combine(const int64_t* keys, const double* vals, int64_t npairs, int
 /* Debugging aid (synchronises the device): out[4] = {runs, work cursor, valid runs,
  * pairs} of the last gp_movement_fold call. */
 int gp_fold_stats(int64_t* out);
+
+/* Debugging aid (synchronises the device): out[8] = scan statistics summed over the
+ * gp_assign_round calls made with flags bit 0 since the last reset: {units with
+ * points, scanned points, candidate source entries, staged candidates, overflow
+ * units, exact evaluations, candidate walk steps, point passes}. */
+int gp_scan_stats(uint64_t* out, int reset);
 
 /* K8  bound audit (kmeans.py:347-365): brute-force n x k recheck of the
  * bound contracts for the active points; out[3] += {audited, violations,

@@ -33,7 +33,7 @@ class AssignArgs(C.Structure):
         ("group_list", vp), ("group_count", vp), ("group_cap", i32), ("group_shift", i32),
         ("workspace", vp), ("workspace_bytes", sz), ("scan_regions", i32), ("grid_n", i32),
         ("grid_start", vp), ("grid_items", vp), ("grid_lo", f64 * 3), ("grid_h", f64),
-        ("inv2_min", f64), ("unit_boxes", vp), ("unit_shift", i32), ("pad1", i32),
+        ("inv2_min", f64), ("unit_boxes", vp), ("unit_shift", i32), ("flags", i32),
     ]
 
 
@@ -42,7 +42,7 @@ class FoldArgs(C.Structure):
         ("X", vp), ("ldx", i64), ("d", i32), ("k", i32), ("order3", i32), ("wmode", i32),
         ("w", vp), ("a", vp), ("n_local", i64), ("pos0", i64), ("n_global", i64),
         ("centers", vp), ("weights_only", i32), ("sums", vp), ("wsum", vp), ("extent", vp),
-        ("objective", vp), ("workspace", vp), ("workspace_bytes", sz),
+        ("objective", vp), ("workspace", vp), ("workspace_bytes", sz), ("list", vp), ("m", i64),
     ]
 
 
@@ -75,6 +75,7 @@ _SIGS = {
     "gp_fold_workspace_bytes": (C.c_int, [i64, i64, i64, C.c_int, C.POINTER(sz)]),
     "gp_movement_fold": (C.c_int, [C.POINTER(FoldArgs), vp]),
     "gp_fold_stats": (C.c_int, [vp]),
+    "gp_scan_stats": (C.c_int, [vp, C.c_int]),
     "gp_fold_export": (C.c_int, [C.POINTER(FoldArgs), vp, vp, vp, vp]),
     "gp_fold_combine_bytes": (C.c_int, [C.c_int, C.POINTER(sz)]),
     "gp_fold_combine": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, sz,
@@ -120,11 +121,12 @@ def check(rc: int, what: str = "") -> None:
 KERNELS_PER_CALL = {
     "gp_box_minmax": 2, "gp_weight_probe": 1, "gp_hilbert_keys": 1, "gp_sort_pairs": 9,
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 3,
-    "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 16,
+    "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
     "gp_group_candidates": 1, "gp_sample_ranks": 90, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
 }
 _launches = [0]
+calls: dict[str, int] = {}   # API calls by name (tools/kprof.py)
 
 
 def reset_launch_count() -> None:
@@ -137,6 +139,7 @@ def launch_count() -> int:
 
 def count(name: str) -> None:
     _launches[0] += KERNELS_PER_CALL.get(name, 0)
+    calls[name] = calls.get(name, 0) + 1
 
 
 def call(name: str, *args) -> None:

@@ -290,6 +290,8 @@ __device__ __forceinline__ double qdist(const double* x, const WarpCand<D>& W, i
   return s * W.i2[i];
 }
 
+__device__ unsigned long long g_scan_stats[8];  // gp_scan_stats (flags bit 0)
+
 constexpr int SREG = 4;            // max filter regions per scan unit (runtime sreg <= SREG)
 constexpr double SEP = 1e-12;      // q separation above which no exact evaluation is needed
 constexpr float AP_HI_F = 1.0f + 2.4e-7f;  // margins of the sqrt(q)-derived float bounds
@@ -398,7 +400,7 @@ __device__ void grid_point(const gp_assign_args& p, const double* x, int& bi, fl
 }
 
 template <int D, int WM>
-__global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
+__global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
                                                    int sreg, const int32_t* __restrict__ scan,
                                                    const int32_t* __restrict__ olda,
                                                    const int32_t* __restrict__ runs) {
@@ -528,6 +530,14 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
     }
     const bool overflow = ncand > CAPW;  // then stream the whole source in chunks
     const int total = overflow ? nsrc : ncand;
+    if ((p.flags & 1) && lane == 0) {
+      atomicAdd(&g_scan_stats[0], 1ull);
+      atomicAdd(&g_scan_stats[1], (unsigned long long)total_pts);
+      atomicAdd(&g_scan_stats[2], (unsigned long long)nsrc);
+      atomicAdd(&g_scan_stats[3], (unsigned long long)ncand);
+      atomicAdd(&g_scan_stats[4], overflow ? 1ull : 0ull);
+      atomicAdd(&g_scan_stats[7], (unsigned long long)((total_pts + 31) / 32));
+    }
     __syncwarp();
     if (!overflow) {
       // rank sort of the staged candidates by (lsq, slot): the per-point walk
@@ -581,6 +591,7 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
           const int i = W.order[t];
           done = done || W.lsq[i] > fma(q2, Q_TOL, q2);
           if (__all_sync(FULL, done)) break;
+          if ((p.flags & 1) && lane == 0) atomicAdd(&g_scan_stats[6], 1ull);
           if (!done) {
             const double qq = qdist<D>(x, W, i);
             const bool l1 = qq < q1, l2 = qq < q2;
@@ -675,7 +686,7 @@ __global__ void __launch_bounds__(STH) scan_kernel(gp_assign_args p, int wshift,
     nexact += __shfl_xor_sync(FULL, nexact, o);
   }
   if (lane == 0 && nq) atomicAdd(&p.counters[2], nq);
-  (void)nexact;
+  if ((p.flags & 1) && lane == 0) atomicAdd(&g_scan_stats[5], nexact);
   __syncthreads();
   for (int i = tid; i < HSLOTS; i += STH)
     if (s_ckey[i] >= 0 && s_cval[i] != 0)
@@ -1060,6 +1071,16 @@ int gp_audit(const gp_assign_args* args, unsigned long long* out, void* stream) 
   if (args->d == 2) audit_kernel<2><<<grid, 128, 0, s>>>(*args, out);
   else audit_kernel<3><<<grid, 128, 0, s>>>(*args, out);
   return check_launch("audit");
+}
+
+int gp_scan_stats(uint64_t* out, int reset) {
+  GP_CUDA(cudaDeviceSynchronize());
+  GP_CUDA(cudaMemcpyFromSymbol(out, g_scan_stats, sizeof(g_scan_stats)));
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    GP_CUDA(cudaMemcpyToSymbol(g_scan_stats, z, sizeof(z)));
+  }
+  return GP_OK;
 }
 
 int gp_group_boxes(const double* X, int64_t ldx, int d, const int32_t* list, int64_t m, int shift,

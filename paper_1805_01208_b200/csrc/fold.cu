@@ -17,6 +17,7 @@
 //              objective terms (kmeans.py:490-499) are computed in parallel
 //              by all lanes of the chunk;
 //   combine  : per block, fold the pair partials in segment order.
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -26,16 +27,19 @@
 
 namespace gp {
 
-constexpr int FT = 256;     // threads per fold CTA (8 warps)
+constexpr int FT = 128;     // threads per fold CTA (4 warps; ~34 KB of staging)
 constexpr int MAXCOL = 5;   // d wx columns + w + objective (d <= 3)
-constexpr int FB = 4;       // chunks of 32 positions prefetched per batch
 
 // counters[]: 0 runs, 1 work cursor, 2 valid runs, 3 pairs
 struct FoldLayout {
-  int64_t s0, nseg, cells, cap, pcap;
+  int64_t s0, nseg, cells, cap, pcap, ntiles;
   size_t off_flags, off_starts, off_rkey, off_skey, off_sidx, off_ridx, off_pbeg, off_slot,
-      off_out, off_counters, off_cub, cub_bytes, off_rpre, off_spos, off_skey_final, total;
+      off_out, off_counters, off_cub, cub_bytes, off_tiles, off_skey_final, total;
 };
+
+constexpr int RT = 256;             // run extraction: threads per tile
+constexpr int RPER = 16;            // positions per thread
+constexpr int RTILE = RT * RPER;    // positions per tile
 
 static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k) {
   FoldLayout L;
@@ -46,9 +50,10 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   L.cells = L.nseg * k;
   L.cap = n_local > 0 ? n_local : 1;
   L.pcap = L.cells < L.cap ? L.cells : L.cap;  // pairs <= min(segments x blocks, runs)
+  L.ntiles = (L.cap + RTILE - 1) / RTILE;
   size_t b1 = 0, b2 = 0, b3 = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, b3, (const int64_t*)nullptr, (int64_t*)nullptr,
-                                (int)L.cap + 1);
+  cub::DeviceScan::ExclusiveSum(nullptr, b3, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                (int)L.ntiles + 1);
   cub::DeviceSelect::Flagged(nullptr, b1, cub::CountingInputIterator<int32_t>(0),
                              (const uint8_t*)nullptr, (int32_t*)nullptr, (int64_t*)nullptr,
                              (int)L.cap);
@@ -71,73 +76,118 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   L.off_out = o; o = al(o + L.pcap * (MAXCOL + 1) * sizeof(double));
   L.off_counters = o; o = al(o + 8 * sizeof(int64_t));
   L.off_cub = o; o = al(o + L.cub_bytes);
-  L.off_rpre = o; o = al(o + (L.cap + 1) * 8);
-  L.off_spos = o; o = al(o + L.cap * 4);
+  L.off_tiles = o; o = al(o + (L.ntiles + 1) * 4);
   L.total = o;
   return L;
 }
 
-__device__ __forceinline__ int32_t fold_key(const int32_t* a, int64_t i, int64_t pos0,
-                                            int64_t n_global, int64_t s0, int k) {
-  int c = a[i];
-  return c >= 0 ? (int32_t)((segment_of(pos0 + i, n_global) - s0) * k + c) : -1;
-}
-
-// flag every position whose key differs from its predecessor's (run starts);
-// each thread handles MK consecutive positions with one segment computation
-constexpr int MK = 8;
-__global__ void fold_mark(const int32_t* __restrict__ a, int64_t n_local, int64_t pos0,
-                          int64_t n_global, int64_t s0, int k, uint8_t* __restrict__ flags) {
-  const int64_t nt = (n_local + MK - 1) / MK;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i0 = t * MK;
-    int seg = segment_of(pos0 + i0, n_global);
-    int64_t next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * n_global >> 8) - pos0
-                                            : INT64_MAX;  // local position of the next segment
-    int prev_key = i0 > 0 ? fold_key(a, i0 - 1, pos0, n_global, s0, k) : -2;
-    uint8_t f[MK];
+// (segment, block) keys of a thread's RPER consecutive entries and the bit mask
+// of those that start a run (key differs from the previous entry's).  Key -1:
+// unassigned / inactive.  Entries are local positions i (list == NULL, one
+// segment computation per thread) or dense entries at positions list[i].
+__device__ __forceinline__ unsigned run_marks(const gp_fold_args& f, int64_t cnt, int64_t s0,
+                                              int64_t i0, int32_t (&key)[RPER]) {
+  int av[RPER];
+  if (i0 + RPER <= cnt) {
+    const int4* ap = reinterpret_cast<const int4*>(f.a + i0);
 #pragma unroll
-    for (int e = 0; e < MK; ++e) {
-      const int64_t i = i0 + e;
-      if (i >= n_local) break;
+    for (int h = 0; h < RPER / 4; ++h) {
+      const int4 v = ap[h];
+      av[4 * h] = v.x; av[4 * h + 1] = v.y; av[4 * h + 2] = v.z; av[4 * h + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < RPER; ++e) av[e] = i0 + e < cnt ? f.a[i0 + e] : -1;
+  }
+  auto seg_at = [&](int64_t i) { return segment_of(f.pos0 + (f.list ? f.list[i] : i), f.n_global); };
+  int prev = -2;
+  if (i0 > 0) {
+    const int c = f.a[i0 - 1];
+    prev = c >= 0 ? (int)((seg_at(i0 - 1) - s0) * f.k + c) : -1;
+  }
+  int seg = 0;
+  int64_t next_b = 0;
+  if (!f.list) {
+    seg = segment_of(f.pos0 + i0, f.n_global);
+    next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * f.n_global >> 8) - f.pos0 : INT64_MAX;
+  }
+  unsigned m = 0;
+#pragma unroll
+  for (int e = 0; e < RPER; ++e) {
+    const int64_t i = i0 + e;
+    if (i >= cnt) {
+      key[e] = -1;
+      continue;
+    }
+    int sg;
+    if (f.list) {
+      sg = av[e] >= 0 ? seg_at(i) : 0;
+    } else {
       while (i >= next_b) {
         ++seg;
-        next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * n_global >> 8) - pos0 : INT64_MAX;
+        next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * f.n_global >> 8) - f.pos0
+                                       : INT64_MAX;
       }
-      const int c = a[i];
-      const int key = c >= 0 ? (int)((seg - s0) * k + c) : -1;
-      f[e] = key != prev_key;
-      prev_key = key;
+      sg = seg;
     }
-    if (i0 + MK <= n_local) {
-      uint2 v;
-      v.x = f[0] | (f[1] << 8) | (f[2] << 16) | ((unsigned)f[3] << 24);
-      v.y = f[4] | (f[5] << 8) | (f[6] << 16) | ((unsigned)f[7] << 24);
-      *reinterpret_cast<uint2*>(flags + i0) = v;
-    } else {
-      for (int e = 0; i0 + e < n_local; ++e) flags[i0 + e] = f[e];
-    }
+    const int kk = av[e] >= 0 ? (int)((sg - s0) * f.k + av[e]) : -1;
+    key[e] = kk;
+    if (kk != prev) m |= 1u << e;
+    prev = kk;
+  }
+  return m;
+}
+
+// pass 1: number of run starts per tile of RTILE entries
+__global__ void __launch_bounds__(RT) run_count(gp_fold_args f, int64_t cnt, int64_t s0,
+                                                int32_t* __restrict__ tiles) {
+  __shared__ int ws[RT / 32];
+  const int64_t i0 = (int64_t)blockIdx.x * RTILE + (int64_t)threadIdx.x * RPER;
+  int32_t key[RPER];
+  int c = i0 < cnt ? __popc(run_marks(f, cnt, s0, i0, key)) : 0;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < RT / 32; ++w) t += ws[w];
+    tiles[blockIdx.x] = t;
   }
 }
 
-// run r -> (key, r); runs with key -1 (unassigned / inactive) sort last
-__global__ void fold_run_keys(const int32_t* __restrict__ a, int32_t* __restrict__ starts,
-                              int64_t R, int64_t* counters, int64_t n_local, int64_t pos0,
-                              int64_t n_global, int64_t s0, int k, uint32_t* __restrict__ rkey,
-                              int32_t* __restrict__ ridx) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) starts[R] = (int32_t)n_local;  // sentinel end
+// pass 2: run r (in entry order) -> starts[r] = first entry, (key, r) for the
+// sort; runs with key -1 (unassigned / inactive) sort last
+__global__ void __launch_bounds__(RT) run_write(gp_fold_args f, int64_t cnt, int64_t s0,
+                                                const int32_t* __restrict__ tile_off,
+                                                int64_t ntiles, int32_t* __restrict__ starts,
+                                                uint32_t* __restrict__ rkey,
+                                                int32_t* __restrict__ ridx, int64_t* counters) {
+  typedef cub::BlockScan<int, RT> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const int64_t i0 = (int64_t)blockIdx.x * RTILE + (int64_t)threadIdx.x * RPER;
+  int32_t key[RPER];
+  const unsigned m = i0 < cnt ? run_marks(f, cnt, s0, i0, key) : 0u;
+  int excl;
+  Scan(tmp).ExclusiveSum(__popc(m), excl);
+  int r = tile_off[blockIdx.x] + excl;
   int valid = 0;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    int32_t key = fold_key(a, starts[r], pos0, n_global, s0, k);
-    rkey[r] = (uint32_t)key;  // -1 -> 0xffffffff
-    ridx[r] = (int32_t)r;
-    valid += key >= 0;
-  }
+#pragma unroll
+  for (int e = 0; e < RPER; ++e)
+    if (m & (1u << e)) {
+      starts[r] = (int32_t)(i0 + e);
+      rkey[r] = (uint32_t)key[e];
+      ridx[r] = r;
+      valid += key[e] >= 0;
+      ++r;
+    }
   for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(FULL, valid, o);
   if ((threadIdx.x & 31) == 0 && valid)
     atomicAdd((unsigned long long*)&counters[2], (unsigned long long)valid);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int R = tile_off[ntiles];
+    starts[R] = (int32_t)cnt;  // sentinel end
+    counters[0] = R;
+  }
 }
 
 // first sorted run of every pair (valid runs occupy the first counters[2] slots)
@@ -149,37 +199,6 @@ __global__ void fold_pair_flags(const uint32_t* __restrict__ skey, int64_t R,
     flags[j] = j < V && (j == 0 || skey[j] != skey[j - 1]);
 }
 
-// length of the j-th sorted run (valid runs only; 0 beyond)
-__global__ void fold_run_len(const int32_t* __restrict__ starts, const int32_t* __restrict__ sidx,
-                             int64_t R, const int64_t* counters, int64_t* __restrict__ len) {
-  const int64_t V = counters[2];
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= R;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    int64_t l = 0;
-    if (j < V) {
-      const int r = sidx[j];
-      l = starts[r + 1] - starts[r];
-    }
-    len[j] = l;
-  }
-}
-
-// sorted positions: every valid position, grouped by pair, in position order
-// within the pair (one warp per sorted run)
-__global__ void fold_expand(const int32_t* __restrict__ starts, const int32_t* __restrict__ sidx,
-                            const int64_t* __restrict__ pre, const int64_t* counters,
-                            int32_t* __restrict__ spos) {
-  const int64_t V = counters[2];
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; j < V; j += nw) {
-    const int r = sidx[j];
-    const int32_t b = starts[r], e = starts[r + 1];
-    const int64_t o = pre[j];
-    for (int32_t t = lane; t < e - b; t += 32) spos[o + t] = b + t;
-  }
-}
-
 __global__ void fold_slots(const uint32_t* __restrict__ skey, int32_t* __restrict__ pbeg,
                            const int64_t* counters, int32_t* __restrict__ slot) {
   const int64_t P = counters[3];
@@ -189,94 +208,133 @@ __global__ void fold_slots(const uint32_t* __restrict__ skey, int32_t* __restric
     slot[skey[pbeg[p]]] = (int32_t)p;
 }
 
-// One warp per (segment, block) pair: its positions (contiguous in spos, in
-// position order) in batches of FB*32; the loads of batch b+1 are issued before
-// batch b is folded, so the serial fold (lane j folds column j) overlaps them.
-template <int D>
-__device__ __forceinline__ void fold_load(const gp_fold_args& f, const int32_t* spos, int64_t v0,
-                                          int64_t v1, int lane, double (&xv)[FB][D],
-                                          double (&wv)[FB]) {
-#pragma unroll
-  for (int b = 0; b < FB; ++b) {
-    const int64_t v = v0 + b * 32 + lane;
-    const bool in = v < v1;
-    const int i = in ? spos[v] : 0;
-    wv[b] = in ? load_weight(f.w, f.wmode, i) : 0.0;
-    if (!f.weights_only) {
-      if (in) load_point<D>(f.X, f.ldx, i, xv[b]);
-      else
-#pragma unroll
-        for (int j = 0; j < D; ++j) xv[b][j] = 0.0;
-    }
-  }
-}
-
-template <int D>
-__global__ void __launch_bounds__(FT) fold_kernel(gp_fold_args f, const int32_t* __restrict__ spos,
-                                                  const int64_t* __restrict__ pre,
+// Pair folds, G = 32 / NC pairs per warp.  Lane g < G owns group g's cursor
+// (pair, sorted run j, entry cur, run end re); each step the whole warp loads
+// up to 32 consecutive entries of every group's current run, computes w*x, w,
+// w*|x-c|^2 (and the max |x-c|^2 for the extent) and stages them in shared
+// memory; then lane (g, col) folds column col of group g in entry order, which
+// is the bincount order of the reference.  A group whose pair ends writes the
+// pair's partials and takes the next pair from the work counter.
+template <int D, int NC>
+__global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t* __restrict__ starts,
+                                                  const int32_t* __restrict__ sidx,
                                                   const uint32_t* __restrict__ skey,
                                                   const int32_t* __restrict__ pbeg,
                                                   int64_t* counters, double* __restrict__ out) {
-  __shared__ double sm[FT / 32][MAXCOL][FB * 32 + 1];
+  constexpr int G = 32 / NC;
+  constexpr int W = FT / 32;
+  __shared__ double st[W][G * NC][33];
+  __shared__ double scen[W][G][D];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ncols = f.weights_only ? 1 : D + 2;
-  const int64_t npairs = counters[3];
-  for (;;) {
-    int64_t pi;
-    if (lane == 0) pi = (int64_t)atomicAdd((unsigned long long*)&counters[1], 1ull);
-    pi = __shfl_sync(FULL, pi, 0);
-    if (pi >= npairs) break;
-    const int j0 = pbeg[pi], j1 = pbeg[pi + 1];
-    const int c = (int)(skey[j0] % (uint32_t)f.k);
-    const int64_t v0 = pre[j0], v1 = pre[j1];
-    double cold[D];
-    if (!f.weights_only) {
-#pragma unroll
-      for (int j = 0; j < D; ++j) cold[j] = f.centers[c * D + j];
+  const int64_t P = counters[3];
+  int pair = -1, j = 0, j1 = 0, cur = 0, re = 0;
+  auto fetch = [&]() {
+    const int64_t pi = (int64_t)atomicAdd((unsigned long long*)&counters[1], 1ull);
+    if (pi >= P) {
+      pair = -1;
+      return;
     }
-    double acc = 0.0;  // lane j < ncols folds column j; bincount starts from 0.0
-    double ext = 0.0;
-    double xv[FB][D], wv[FB];
-    fold_load<D>(f, spos, v0, v1, lane, xv, wv);
-    for (int64_t base = v0; base < v1; base += FB * 32) {
-      // stage the current batch, then issue the next batch's loads
+    pair = (int)pi;
+    j = pbeg[pi];
+    j1 = pbeg[pi + 1];
+    const int r = sidx[j];
+    cur = starts[r];
+    re = starts[r + 1];
+    if (NC > 1) {
+      const int c = (int)(skey[j] % (uint32_t)f.k);
 #pragma unroll
-      for (int b = 0; b < FB; ++b) {
-        const int slot = b * 32 + lane;
-        const bool in = base + slot < v1;
-        if (f.weights_only) {
-          sm[warp][0][slot] = wv[b];
+      for (int q = 0; q < D; ++q) scen[warp][lane][q] = f.centers[c * D + q];
+    }
+  };
+  if (lane < G) fetch();
+  __syncwarp();
+  const int mg = lane / NC, col = lane - mg * NC;
+  double acc = 0.0;  // bincount starts from 0.0
+  double extg[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) extg[g] = 0.0;
+  for (;;) {
+    const bool live = lane < G && pair >= 0;
+    const int cnt = live ? min(32, re - cur) : 0;
+    if (!__any_sync(FULL, live)) break;
+    // all groups' loads first (clamped to a valid entry), so they are in flight together
+    int ngs[G];
+    double xr[G][D], wr[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int cg = __shfl_sync(FULL, cur, g);
+      ngs[g] = __shfl_sync(FULL, cnt, g);
+      const int i = ngs[g] > 0 ? cg + min(lane, ngs[g] - 1) : 0;
+      wr[g] = load_weight(f.w, f.wmode, i);
+      if (NC > 1) load_point<D>(f.X, f.ldx, i, xr[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (lane < ngs[g]) {
+        const double w = wr[g];
+        if (NC == 1) {
+          st[warp][g][lane] = w;
         } else {
           double diff[D];
 #pragma unroll
-          for (int j = 0; j < D; ++j) {
-            sm[warp][j][slot] = __dmul_rn(xv[b][j], wv[b]);  // wx = points * weights[:, None]
-            diff[j] = __dsub_rn(xv[b][j], cold[j]);
+          for (int q = 0; q < D; ++q) {
+            st[warp][g * NC + q][lane] = __dmul_rn(xr[g][q], w);  // wx = points * weights[:, None]
+            diff[q] = __dsub_rn(xr[g][q], scen[warp][g][q]);
           }
           const double sq = sqnorm_rn(diff, D, f.order3);
-          sm[warp][D][slot] = wv[b];
-          sm[warp][D + 1][slot] = __dmul_rn(sq, wv[b]);
-          if (in) ext = fmax(ext, __dsqrt_rn(sq));
+          st[warp][g * NC + D][lane] = w;
+          st[warp][g * NC + D + 1][lane] = __dmul_rn(sq, w);
+          extg[g] = fmax(extg[g], sq);  // sqrt is monotone: max of sqrt = sqrt of max
         }
       }
-      __syncwarp();
-      if (base + FB * 32 < v1) fold_load<D>(f, spos, base + FB * 32, v1, lane, xv, wv);
-      const int cnt = (int)min((int64_t)(FB * 32), v1 - base);
-      if (lane < ncols) {
-        const double* col = sm[warp][lane];
-        if (cnt == FB * 32) {
-#pragma unroll 32
-          for (int t = 0; t < FB * 32; ++t) acc = __dadd_rn(acc, col[t]);
+    }
+    __syncwarp();
+    const int nmine = __shfl_sync(FULL, cnt, mg < G ? mg : 0);
+    if (mg < G) {
+      const double* colp = st[warp][mg * NC + col];
+      if (nmine == 32) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) acc = __dadd_rn(acc, colp[t]);
+      } else {
+        for (int t = 0; t < nmine; ++t) acc = __dadd_rn(acc, colp[t]);
+      }
+    }
+    __syncwarp();
+    bool done = false;
+    if (live) {
+      cur += cnt;
+      if (cur >= re) {
+        ++j;
+        if (j < j1) {
+          const int r = sidx[j];
+          cur = starts[r];
+          re = starts[r + 1];
         } else {
-          for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, col[t]);
+          done = true;
         }
       }
+    }
+    const unsigned dm = __ballot_sync(FULL, done);
+    if (dm) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (!(dm & (1u << g))) continue;
+        const int pg = __shfl_sync(FULL, pair, g);
+        double* po = out + (int64_t)pg * (MAXCOL + 1);
+        if (mg == g) {
+          po[col] = acc;
+          acc = 0.0;
+        }
+        if (NC > 1) {
+          double e = extg[g];
+          for (int o = 16; o; o >>= 1) e = fmax(e, __shfl_xor_sync(FULL, e, o));
+          if (lane == 0) po[MAXCOL] = __dsqrt_rn(e);
+          extg[g] = 0.0;
+        }
+      }
+      if (done) fetch();
       __syncwarp();
     }
-    for (int o = 16; o; o >>= 1) ext = fmax(ext, __shfl_xor_sync(FULL, ext, o));
-    double* po = out + pi * (MAXCOL + 1);
-    if (lane < ncols) po[lane] = acc;
-    if (lane == 0) po[MAXCOL] = ext;
   }
 }
 
@@ -411,6 +469,7 @@ int gp_fold_workspace_bytes(int64_t n_local, int64_t pos0, int64_t n_global, int
 int gp_movement_fold(const gp_fold_args* f, void* stream) {
   GP_REQUIRE(f && (f->d == 2 || f->d == 3) && f->k >= 1, "gp_movement_fold: bad args");
   GP_REQUIRE(f->n_local >= 0 && f->n_local < (1ll << 31), "gp_movement_fold: n out of range");
+  GP_REQUIRE(!f->list || (f->m >= 0 && f->m <= f->n_local), "gp_movement_fold: m out of range");
   GP_REQUIRE(f->wmode == GP_W_UNIT || f->w != nullptr, "gp_movement_fold: weights missing");
   GP_REQUIRE(f->wsum != nullptr, "gp_movement_fold: wsum missing");
   GP_REQUIRE(f->weights_only || (f->sums && f->extent && f->objective && f->centers),
@@ -431,33 +490,35 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
   int32_t* slot = (int32_t*)(ws + L.off_slot);
   double* out = (double*)(ws + L.off_out);
   int64_t* counters = (int64_t*)(ws + L.off_counters);
-  int64_t* rpre = (int64_t*)(ws + L.off_rpre);
-  int32_t* spos = (int32_t*)(ws + L.off_spos);
+  int32_t* tiles = (int32_t*)(ws + L.off_tiles);
   g_last_counters = counters;
   void* cub_tmp = ws + L.off_cub;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t n = f->n_local;
+  const int64_t cnt = f->list ? f->m : f->n_local;   // entries
 
   GP_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(int64_t), s));
   GP_CUDA(cudaMemsetAsync(slot, 0xff, L.cells * sizeof(int32_t), s));
-  if (n > 0) {
-    fold_mark<<<grid_for((n + MK - 1) / MK, 256, sms * 16), 256, 0, s>>>(f->a, n, f->pos0, f->n_global, L.s0,
-                                                          f->k, flags);
+  if (cnt > 0) {
+    const int64_t nt = (cnt + RTILE - 1) / RTILE;
+    run_count<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, tiles);
+    GP_CUDA(cudaMemsetAsync(tiles + nt, 0, sizeof(int32_t), s));
     size_t b = L.cub_bytes;
-    GP_CUDA(cub::DeviceSelect::Flagged(cub_tmp, b, cub::CountingInputIterator<int32_t>(0), flags,
-                                       starts, counters + 0, (int)n, s));
+    GP_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, b, tiles, tiles, (int)nt + 1, s));
+    run_write<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, tiles, nt, starts, rkey, ridx, counters);
     int64_t R = 0;
     GP_CUDA(cudaMemcpyAsync(&R, counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     GP_CUDA(cudaStreamSynchronize(s));
-    fold_run_keys<<<grid_for(R, 256, sms * 16), 256, 0, s>>>(
-        f->a, starts, R, counters, n, f->pos0, f->n_global, L.s0, f->k, rkey, ridx);
     // stable LSD radix sort with ping-pong buffers (no n-sized CUB scratch)
     cub::DoubleBuffer<uint32_t> kb(rkey, skey);
     cub::DoubleBuffer<int32_t> vb(ridx, sidx);
     b = L.cub_bytes;
-    GP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, b, kb, vb, (int)R, 0, 32, s));
+    int bits = 1;
+    while (bits < 32 && ((uint64_t)L.cells >> bits) != 0) ++bits;
+    // valid keys are < cells < 2^bits and invalid ones (0xffffffff) are all-ones in
+    // the low `bits` bits, so sorting those bits keeps the invalid runs last
+    GP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, b, kb, vb, (int)R, 0, bits, s));
     skey = kb.Current();
     sidx = vb.Current();
     if (skey != (uint32_t*)(ws + L.off_skey_final)) {
@@ -471,20 +532,25 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     GP_CUDA(cub::DeviceSelect::Flagged(cub_tmp, b, cub::CountingInputIterator<int32_t>(0), flags,
                                        pbeg, counters + 3, (int)R, s));
     fold_slots<<<grid_for(R, 256, sms * 8), 256, 0, s>>>(skey, pbeg, counters, slot);
-    // positions grouped by pair: prefix of the sorted run lengths, then expansion
-    fold_run_len<<<grid_for(R + 1, 256, sms * 8), 256, 0, s>>>(starts, sidx, R, counters, rpre);
-    b = L.cub_bytes;
-    GP_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, b, rpre, rpre, (int)(R + 1), s));
-    fold_expand<<<grid_for(R * 32, 256, sms * 16), 256, 0, s>>>(starts, sidx, rpre, counters,
-                                                                spos);
   }
-  if (f->d == 2) {
-    fold_kernel<2><<<sms * 6, FT, 0, s>>>(*f, spos, rpre, skey, pbeg, counters, out);
-    fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
+  int per_sm = 1;
+  if (f->weights_only) {
+    if (f->d == 2) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<2, 1>, FT, 0);
+      fold_groups<2, 1><<<sms * per_sm, FT, 0, s>>>(*f, starts, sidx, skey, pbeg, counters, out);
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<3, 1>, FT, 0);
+      fold_groups<3, 1><<<sms * per_sm, FT, 0, s>>>(*f, starts, sidx, skey, pbeg, counters, out);
+    }
+  } else if (f->d == 2) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<2, 4>, FT, 0);
+    fold_groups<2, 4><<<sms * per_sm, FT, 0, s>>>(*f, starts, sidx, skey, pbeg, counters, out);
   } else {
-    fold_kernel<3><<<sms * 6, FT, 0, s>>>(*f, spos, rpre, skey, pbeg, counters, out);
-    fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<3, 5>, FT, 0);
+    fold_groups<3, 5><<<sms * per_sm, FT, 0, s>>>(*f, starts, sidx, skey, pbeg, counters, out);
   }
+  if (f->d == 2) fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
+  else fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   return check_launch("movement_fold");
 }
 

@@ -101,6 +101,7 @@ class _Timer:
     def __init__(self):
         self.events = []
         self.rounds = []   # (n_active, n_scanned, n_evals) per assign launch
+        self.scan = []     # gp_scan_stats per round (GP_SCAN_STATS=1)
 
     def mark(self, stream):
         ev = torch.cuda.Event(enable_timing=True)
@@ -352,6 +353,8 @@ class DevicePartitioner:
         awb = N.size_query("gp_assign_workspace_bytes", n)
         self.assign_ws = torch.empty(awb, dtype=torch.uint8, device=dev)
         a.workspace, a.workspace_bytes = self.assign_ws.data_ptr(), awb
+        # scan statistics for tools/kprof.py (debugging aid; costs a sync per round)
+        a.flags = 1 if self.timer is not None and os.environ.get("GP_SCAN_STATS") else 0
         self.aargs = a
         self.hier = _Hierarchy(self, use_mega=k > 4096) if k > 128 else None
         f = N.FoldArgs()
@@ -464,9 +467,12 @@ class DevicePartitioner:
         self.dense_m = m
 
     def _leave_dense(self):
-        """Write the dense sample state back and point the kernels at the full arrays."""
+        """Write the dense sample state back and point the kernels at the full arrays.
+        The movement fold that follows still reads the dense arrays (gp_fold_args.list)."""
         if not getattr(self, "dense_m", 0):
+            self.fold_dense = None
             return
+        self.fold_dense = self.dense_m
         N.call("gp_scatter_state", self.active_idx.data_ptr(), self.dense_m, self.A_d.data_ptr(),
                self.UBLB_d.data_ptr(), self.A.data_ptr(), self.UBLB.data_ptr(), self.sh)
         a = self.aargs
@@ -507,6 +513,10 @@ class DevicePartitioner:
         cnt[1] = self.m_global  # every active entry is one decision (kmeans.py:309)
         if self.timer is not None:
             self.timer.rounds.append((int(cnt[1]), int(cnt[1] - cnt[0]), int(cnt[2])))
+            if self.aargs.flags & 1:
+                st = np.zeros(8, dtype=np.uint64)
+                N.check(N.lib.gp_scan_stats(st.ctypes.data, 1), "gp_scan_stats")
+                self.timer.scan.append(st)
         return host[:k].copy(), cnt
 
     # ---- hooks the multi-GPU partitioner overrides (one shard: nothing to exchange)
@@ -522,6 +532,14 @@ class DevicePartitioner:
     def _fold(self, weights_only):
         f = self.fargs
         f.weights_only = weights_only
+        m = getattr(self, "fold_dense", None) if not weights_only else None
+        if m:
+            # warm-up sample: fold the dense active entries (SFC order) at their positions
+            f.X, f.a, f.w = self.X_d.data_ptr(), self.A_d.data_ptr(), _ptr(self.W_d)
+            f.list, f.m = self.active_idx.data_ptr(), m
+        else:
+            f.X, f.a, f.w = self.X.data_ptr(), self.A.data_ptr(), _ptr(self.W)
+            f.list, f.m = None, 0
         N.count("gp_movement_fold")
         N.check(N.lib.gp_movement_fold(C.byref(f), self.sh), "gp_movement_fold")
 

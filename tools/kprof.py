@@ -19,6 +19,8 @@ c, pts_d, w_d, _ = bench.device_workload(cfg, dev)
 s = KMeansSettings(k=c["k"], epsilon=c["epsilon"], seed=0)
 partition_device(pts_d, w_d, s, device=dev)  # warm
 torch.cuda.synchronize()
+N0 = __import__("paper_1805_01208_b200._native", fromlist=["calls"])
+N0.calls.clear()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     out, stats = partition_device(pts_d, w_d, s, device=dev)
     torch.cuda.synchronize()
@@ -30,6 +32,7 @@ for e in prof.events():
     r[0] += 1
     r[1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
 tot = sum(v[1] for v in rows.values())
+print("API calls:", dict(sorted(N0.calls.items())))
 print(f"{'kernel':72s} {'calls':>6s} {'ms':>10s} {'%':>6s}")
 for k, v in sorted(rows.items(), key=lambda x: -x[1][1])[:25]:
     print(f"{k:72s} {v[0]:6d} {v[1] / 1e3:10.2f} {100 * v[1] / tot:6.1f}")
@@ -41,6 +44,7 @@ for r in stats.iterations[::4] + stats.iterations[-3:]:
     print(r.phase, r.active_points, r.balance_rounds, sc // max(r.balance_rounds, 1),
           round(r.distance_evals / max(sc, 1), 2))
 
+os.environ["GP_SCAN_STATS"] = "1"
 t = _Timer()
 out, stats = partition_device(pts_d, w_d, s, device=dev, timer=t)
 torch.cuda.synchronize()
@@ -64,3 +68,16 @@ for ms_, r in zip(ms, t.rounds):
 print("active  rounds  ms  ms/round  scanned/round  qevals/scanned")
 for m_, e in sorted(by.items()):
     print(m_, e[0], round(e[1], 1), round(e[1] / e[0], 3), e[2] // e[0], round(e[3] / max(e[2], 1), 1))
+
+if t.scan:
+    print("scan stats per active size: units  pts/unit  nsrc/unit  ncand/unit  overflow%  "
+          "exact/pt  walk/pass  passes/unit")
+    by = {}
+    for st_, r in zip(t.scan, t.rounds):
+        e = by.setdefault(r[0], np.zeros(8, dtype=np.float64))
+        e += st_.astype(np.float64)
+    for m_, e in sorted(by.items()):
+        u = max(e[0], 1)
+        print(m_, int(e[0]), round(e[1] / u, 1), round(e[2] / u, 1), round(e[3] / u, 1),
+              round(100 * e[4] / u, 2), round(e[5] / max(e[1], 1), 3),
+              round(e[6] / max(e[7], 1), 1), round(e[7] / u, 2))
