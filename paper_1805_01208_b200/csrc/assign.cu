@@ -450,6 +450,10 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       return (unit * sreg + r) * WREG + (v - rb);
     };
     auto pos_of = [&](int v) { return scan[slot_of(v)]; };
+    // software pipeline of the passes: positions two passes ahead, coordinates one
+    // pass ahead; the first pass's loads overlap the candidate selection below
+    int qA = lane < total_pts ? pos_of(lane) : 0;
+    int qB = 32 + lane < total_pts ? pos_of(32 + lane) : 0;
     // candidate source: the group's hierarchical list, or all k centers
     const int32_t* src = nullptr;
     int nsrc = p.k;
@@ -530,6 +534,8 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
     }
     const bool overflow = ncand > CAPW;  // then stream the whole source in chunks
     const int total = overflow ? nsrc : ncand;
+    double xA[D];
+    load_point<D>(p.X, p.ldx, qA, xA);  // first pass's coordinates (q = 0 when unused)
     if ((p.flags & 1) && lane == 0) {
       atomicAdd(&g_scan_stats[0], 1ull);
       atomicAdd(&g_scan_stats[1], (unsigned long long)total_pts);
@@ -577,9 +583,16 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
     for (int pb = 0; pb < total_pts; pb += 32) {
       const int v = pb + lane;
       const bool valid = v < total_pts;
-      const int q = valid ? pos_of(v) : 0;
+      const int q = valid ? qA : 0;
+      const int oa = valid ? olda[slot_of(v)] : -1;
       double x[D];
-      load_point<D>(p.X, p.ldx, q, x);  // q = 0 for invalid lanes (harmless)
+#pragma unroll
+      for (int j = 0; j < D; ++j) x[j] = xA[j];
+      if (pb + 32 < total_pts) {
+        qA = qB;
+        load_point<D>(p.X, p.ldx, qA, xA);
+        qB = pb + 64 + lane < total_pts ? pos_of(pb + 64 + lane) : 0;
+      }
       // single pass: the two smallest q = d^2/infl^2 with their slots, and the third value
       double q1 = INFINITY, q2 = INFINITY, q3 = INFINITY;
       int i1 = -1, i2 = -1;
@@ -666,7 +679,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       int c = -1;
       if (valid) {
         c = bi;
-        if (olda[slot_of(v)] != c) p.a[q] = c;   // most rescans keep their block
+        if (oa != c) p.a[q] = c;   // most rescans keep their block
         store_bounds(p, q, c, bestf, secondf);
         wv = weight_units<WM>(p.w, q, wshift);
       }
