@@ -103,7 +103,7 @@ constexpr int FCHUNK = FTH * FPER;    // entries per CTA chunk (2048 = 8 regions
 
 struct AssignLayout {
   int64_t nchunks, nregions;
-  size_t off_list, off_olda, off_runs, total;
+  size_t off_list, off_olda, off_runs, off_sched, total;
 };
 
 static AssignLayout assign_layout(int64_t m) {
@@ -116,6 +116,7 @@ static AssignLayout assign_layout(int64_t m) {
   L.off_list = o; o = al(o + (size_t)L.nregions * WREG * 4);
   L.off_olda = o; o = al(o + (size_t)L.nregions * WREG * 4);
   L.off_runs = o; o = al(o + (size_t)L.nregions * 4);
+  L.off_sched = o; o = al(o + 8);
   L.total = o;
   return L;
 }
@@ -129,10 +130,12 @@ template <int WM>
 __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshift, int64_t nchunks,
                                                      int32_t* __restrict__ scan,
                                                      int32_t* __restrict__ olda,
-                                                     int32_t* __restrict__ runs) {
+                                                     int32_t* __restrict__ runs,
+                                                     unsigned long long* __restrict__ sched) {
   __shared__ int s_ckey[HSLOTS];
   __shared__ long long s_cval[HSLOTS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.x == 0 && tid == 0) *sched = 0;  // the scan's work counter
   for (int i = tid; i < HSLOTS; i += FTH) {
     s_ckey[i] = -1;
     s_cval[i] = 0;
@@ -292,6 +295,7 @@ __device__ __forceinline__ double qdist(const double* x, const WarpCand<D>& W, i
 
 __device__ unsigned long long g_scan_stats[8];  // gp_scan_stats (flags bit 0)
 
+constexpr int UCH = 4;             // scan units per scheduler claim (large rounds)
 constexpr int SREG = 4;            // max filter regions per scan unit (runtime sreg <= SREG)
 constexpr double SEP = 1e-12;      // q separation above which no exact evaluation is needed
 constexpr float AP_HI_F = 1.0f + 2.4e-7f;  // margins of the sqrt(q)-derived float bounds
@@ -403,7 +407,9 @@ template <int D, int WM>
 __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
                                                    int sreg, const int32_t* __restrict__ scan,
                                                    const int32_t* __restrict__ olda,
-                                                   const int32_t* __restrict__ runs) {
+                                                   const int32_t* __restrict__ runs,
+                                                   unsigned long long* __restrict__ sched,
+                                                   int uch) {
   __shared__ WarpCand<D> WCs[STH / 32];
   __shared__ int s_ckey[HSLOTS];
   __shared__ long long s_cval[HSLOTS];
@@ -416,14 +422,28 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
   __syncthreads();
   unsigned long long nq = 0, nexact = 0;
   const int64_t nunits = (nregions + sreg - 1) / sreg;
-  const int64_t nwarps = (int64_t)gridDim.x * (STH / 32);
-  int64_t unit = blockIdx.x * (int64_t)(STH / 32) + warp;
+  // dynamic schedule: warps take chunks of UCH consecutive units from a counter (the
+  // next chunk is claimed one chunk ahead), so no warp idles while others finish
+  auto grab = [&]() -> int64_t {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(sched, 1ull);
+    return (int64_t)__shfl_sync(FULL, c, 0) * uch;
+  };
+  int64_t unit = grab(), next_chunk = grab();
   // counts of the unit's regions (lane r < sreg holds region r's), prefetched one unit ahead
   int my_cnt = (unit < nunits && lane < sreg && unit * sreg + lane < nregions)
                    ? runs[unit * sreg + lane] : 0;
-  for (; unit < nunits; unit += nwarps) {
+  int64_t cur_g = -1;          // group whose candidate list src / nsrc hold
+  const int32_t* src = nullptr;
+  int nsrc = p.k;
+  for (int64_t nxt; unit < nunits; unit = nxt) {
     const int cnt_here = my_cnt;
-    const int64_t nxt = unit + nwarps;
+    if ((unit + 1) % uch != 0 && unit + 1 < nunits) {
+      nxt = unit + 1;
+    } else {
+      nxt = next_chunk;
+      if (nxt < nunits) next_chunk = grab();
+    }
     my_cnt = (nxt < nunits && lane < sreg && nxt * sreg + lane < nregions)
                  ? runs[nxt * sreg + lane] : 0;
     // prefix over the SREG region counts (lanes 0..SREG-1)
@@ -455,14 +475,13 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
     int qA = lane < total_pts ? pos_of(lane) : 0;
     int qB = 32 + lane < total_pts ? pos_of(32 + lane) : 0;
     // candidate source: the group's hierarchical list, or all k centers
-    const int32_t* src = nullptr;
-    int nsrc = p.k;
     if (p.group_list) {
       const int64_t g = (unit * sreg * WREG) >> p.group_shift;
-      const int gc = p.group_count[g];
-      if (gc >= 0) {
-        src = p.group_list + g * (int64_t)p.group_cap;
-        nsrc = gc;
+      if (g != cur_g) {   // consecutive units mostly share their group
+        cur_g = g;
+        const int gc = p.group_count[g];
+        src = gc >= 0 ? p.group_list + g * (int64_t)p.group_cap : nullptr;
+        nsrc = gc >= 0 ? gc : p.k;
       }
     }
     // ---- box: the unit's static box (all its active entries), or the box of the
@@ -684,7 +703,10 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
         wv = weight_units<WM>(p.w, q, wshift);
       }
       const unsigned grp = __match_any_sync(FULL, c);
-      if (grp == FULL && valid) {
+      if (WM == GP_W_UNIT) {
+        // one shared-memory add per block present in the pass
+        if (valid && lane == __ffs(grp) - 1) cache_add(s_ckey, s_cval, p.block_w, c, __popc(grp));
+      } else if (grp == FULL && valid) {
         long long g = wv;
         for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(FULL, g, o);
         if (lane == 0) cache_add(s_ckey, s_cval, p.block_w, c, g);
@@ -996,9 +1018,10 @@ static int g_sreg = 0;  // 0: automatic (GP_SCAN_REGIONS overrides)
 
 template <int WM>
 static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout& L,
-                         int32_t* scan, int32_t* olda, int32_t* runs, cudaStream_t s) {
+                         int32_t* scan, int32_t* olda, int32_t* runs,
+                         unsigned long long* sched, cudaStream_t s) {
   unsigned gf = persistent_grid((const void*)filter_kernel<WM>, FTH, L.nchunks);
-  filter_kernel<WM><<<gf, FTH, 0, s>>>(*a, wshift, L.nchunks, scan, olda, runs);
+  filter_kernel<WM><<<gf, FTH, 0, s>>>(*a, wshift, L.nchunks, scan, olda, runs, sched);
   if (g_sreg == 0) {
     const char* e = getenv("GP_SCAN_REGIONS");
     g_sreg = e ? atoi(e) : -1;
@@ -1008,12 +1031,19 @@ static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout
                        : (a->scan_regions > 0 ? a->scan_regions : (a->list ? 1 : SREG));
   if (sreg > SREG) sreg = SREG;
   const int64_t wgroups = (L.nregions + sreg * (STH / 32) - 1) / (sreg * (STH / 32));
+  // consecutive units per claim only when there are many more units than warps (few,
+  // heavy units of a small warm-up sample go one per warp)
+  const int64_t nunits = (L.nregions + sreg - 1) / sreg;
   if (a->d == 2) {
     unsigned gs = persistent_grid((const void*)scan_kernel<2, WM>, STH, wgroups);
-    scan_kernel<2, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs);
+    const int uch = nunits >= 16ll * gs * (STH / 32) ? UCH : 1;
+    scan_kernel<2, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs, sched,
+                                          uch);
   } else {
     unsigned gs = persistent_grid((const void*)scan_kernel<3, WM>, STH, wgroups);
-    scan_kernel<3, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs);
+    const int uch = nunits >= 16ll * gs * (STH / 32) ? UCH : 1;
+    scan_kernel<3, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs, sched,
+                                          uch);
   }
 }
 
@@ -1050,9 +1080,11 @@ int gp_assign_round(const gp_assign_args* args, void* stream) {
   int32_t* scan = (int32_t*)(ws + L.off_list);
   int32_t* olda = (int32_t*)(ws + L.off_olda);
   int32_t* runs = (int32_t*)(ws + L.off_runs);
-  if (args->wmode == GP_W_UNIT) launch_round<GP_W_UNIT>(args, wshift, L, scan, olda, runs, s);
-  else if (args->wmode == GP_W_F32) launch_round<GP_W_F32>(args, wshift, L, scan, olda, runs, s);
-  else launch_round<GP_W_F64>(args, wshift, L, scan, olda, runs, s);
+  unsigned long long* sched = (unsigned long long*)(ws + L.off_sched);
+  if (args->wmode == GP_W_UNIT) launch_round<GP_W_UNIT>(args, wshift, L, scan, olda, runs, sched, s);
+  else if (args->wmode == GP_W_F32)
+    launch_round<GP_W_F32>(args, wshift, L, scan, olda, runs, sched, s);
+  else launch_round<GP_W_F64>(args, wshift, L, scan, olda, runs, sched, s);
   return check_launch("assign_round");
 }
 

@@ -44,10 +44,14 @@ for r in stats.iterations[::4] + stats.iterations[-3:]:
     print(r.phase, r.active_points, r.balance_rounds, sc // max(r.balance_rounds, 1),
           round(r.distance_evals / max(sc, 1), 2))
 
-os.environ["GP_SCAN_STATS"] = "1"
 t = _Timer()
 out, stats = partition_device(pts_d, w_d, s, device=dev, timer=t)
 torch.cuda.synchronize()
+os.environ["GP_SCAN_STATS"] = "1"     # separate run: the statistics cost atomics
+t2 = _Timer()
+partition_device(pts_d, w_d, s, device=dev, timer=t2)
+torch.cuda.synchronize()
+t.scan = t2.scan
 ms = [a.elapsed_time(b) for a, b in t.events]
 full = [(m, r) for m, r in zip(ms, t.rounds) if r[0] == c["n"]]
 samp = [(m, r) for m, r in zip(ms, t.rounds) if r[0] != c["n"]]
