@@ -18,12 +18,12 @@
 // The result per point is the lowest-index argmin of the reference's
 // effective distance, bit for bit; pruning only decides what is evaluated.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace gp {
 
-constexpr int HSLOTS = 128;        // per-CTA block-weight cache
 constexpr double LO_SLACK = 1.0 - 1e-12;
 constexpr double HI_SLACK = 1.0 + 1e-12;
 constexpr double Q_TOL = 1e-13;    // prefilter tolerance (>> the q rounding error)
@@ -65,12 +65,56 @@ __device__ __forceinline__ void store_bounds(const gp_assign_args& p, int64_t q,
       make_float2(ub_normf(N, b_up), lb_normf(p.lb_par[2], p.lb_par[3], s_dn));
 }
 
-__device__ __forceinline__ void cache_add(int* ckey, long long* cval, long long* global, int a,
-                                          long long v) {
-  int slot = a & (HSLOTS - 1);
-  int old = atomicCAS(&ckey[slot], -1, a);
-  if (old == -1 || old == a) atomicAdd((unsigned long long*)&cval[slot], (unsigned long long)v);
-  else atomicAdd((unsigned long long*)&global[a], (unsigned long long)v);
+// Per-warp block-weight table (no atomics, no cross-warp contention): the lanes'
+// (block, value) pairs are combined per distinct block in a warp-uniform loop and
+// one leader lane updates the warp's table; an evicted entry goes to global memory.
+constexpr int WT = 16;
+struct WarpTab {
+  int key[WT];
+  long long val[WT];
+};
+__device__ __forceinline__ void tab_init(WarpTab& t, int lane) {
+  if (lane < WT) {
+    t.key[lane] = -1;
+    t.val[lane] = 0;
+  }
+  __syncwarp();
+}
+template <typename V>
+__device__ __forceinline__ void tab_add(WarpTab& t, long long* global, int lane, bool active,
+                                        int key, V val) {
+  unsigned pend = __ballot_sync(FULL, active);
+  while (pend) {
+    const int leader = __ffs(pend) - 1;
+    const int k = __shfl_sync(FULL, key, leader);
+    const bool mine = active && key == k;
+    const unsigned m = __ballot_sync(FULL, mine);
+    long long sum;
+    if (sizeof(V) == 4) {
+      sum = (long long)__reduce_add_sync(FULL, mine ? (unsigned)val : 0u);
+    } else {
+      sum = mine ? (long long)val : 0;
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+    }
+    if (lane == leader) {
+      const int sl = k & (WT - 1);
+      if (t.key[sl] == k) {
+        t.val[sl] += sum;
+      } else {
+        if (t.key[sl] >= 0)
+          atomicAdd((unsigned long long*)&global[t.key[sl]], (unsigned long long)t.val[sl]);
+        t.key[sl] = k;
+        t.val[sl] = sum;
+      }
+    }
+    __syncwarp();
+    pend &= ~m;
+  }
+}
+__device__ __forceinline__ void tab_flush(WarpTab& t, long long* global, int lane) {
+  __syncwarp();
+  if (lane < WT && t.key[lane] >= 0 && t.val[lane] != 0)
+    atomicAdd((unsigned long long*)&global[t.key[lane]], (unsigned long long)t.val[lane]);
 }
 
 // weight in exact integer units of 1/wscale without fp->int conversions
@@ -121,54 +165,123 @@ static AssignLayout assign_layout(int64_t m) {
   return L;
 }
 
-// Region r = entries [r*WREG, (r+1)*WREG), owned by one warp (8 consecutive
-// entries per lane, 16-byte vector loads in the full phase); its scanned
-// positions go to scan[r*WREG ..] and runs[r] = their count.  Persistent CTAs
-// walk contiguous chunk ranges, so the per-CTA block-weight cache sees few
-// blocks; no CTA-wide barrier inside the loop.
+// Region r = entries [r*WREG, (r+1)*WREG), owned by one warp.  Lane l owns the
+// entry pairs 64h + 2l + {0,1} (h < 4): every warp-wide access is one contiguous
+// 256/512-byte line, in global and in shared memory (no bank conflicts).  Its
+// scanned positions go, in entry order, to scan[r*WREG ..] and runs[r] = their
+// count.  Persistent CTAs walk contiguous chunk ranges (warp w takes region w of
+// every chunk).  Dense full regions are streamed by the bulk-copy engine into a
+// per-warp ring of FSTAGES shared-memory stages (lane 0 issues cp.async.bulk,
+// completion on the stage's mbarrier), so each warp's HBM stream runs ahead of it
+// with no CTA-wide barrier; other regions (sparse lists, the tail) use direct loads.
+constexpr int FSTAGES = 2;
+constexpr int FREG_BYTES = WREG * 12;   // a (4 B) + (ub, lb) (8 B) per entry
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 template <int WM>
 __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshift, int64_t nchunks,
                                                      int32_t* __restrict__ scan,
                                                      int32_t* __restrict__ olda,
                                                      int32_t* __restrict__ runs,
                                                      unsigned long long* __restrict__ sched) {
-  __shared__ int s_ckey[HSLOTS];
-  __shared__ long long s_cval[HSLOTS];
+  typedef typename std::conditional<WM == GP_W_UNIT, int, long long>::type RunW;
+  extern __shared__ __align__(128) unsigned char fsm[];   // [warp][stage] regions
+  __shared__ __align__(8) uint64_t s_bar[FTH / 32][FSTAGES];
+  __shared__ WarpTab s_tab[FTH / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  WarpTab& tab = s_tab[warp];
   if (blockIdx.x == 0 && tid == 0) *sched = 0;  // the scan's work counter
-  for (int i = tid; i < HSLOTS; i += FTH) {
-    s_ckey[i] = -1;
-    s_cval[i] = 0;
-  }
-  __syncthreads();
+  tab_init(tab, lane);
   const int64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
   const int64_t cb = blockIdx.x * per, ce = min(nchunks, cb + per);
+  // regions of chunks [cb, fe) are dense and full: streamed through shared memory
+  const int64_t nfull = p.list == nullptr ? p.m / FCHUNK : 0;
+  const int64_t fe = max(cb, min(ce, nfull));
+  unsigned char* wsm = fsm + (size_t)warp * FSTAGES * FREG_BYTES;
+  auto issue = [&](int64_t c, int sg) {
+    const int64_t e0 = (c * (FCHUNK / WREG) + warp) * WREG;
+    unsigned char* base = wsm + (size_t)sg * FREG_BYTES;
+    mbar_expect_tx(&s_bar[warp][sg], FREG_BYTES);
+    bulk_g2s(base, p.a + e0, WREG * 4, &s_bar[warp][sg]);
+    bulk_g2s(base + WREG * 4, p.ublb + 2 * e0, WREG * 8, &s_bar[warp][sg]);
+  };
+  if (lane == 0) {
+    for (int sg = 0; sg < FSTAGES; ++sg) mbar_init(&s_bar[warp][sg], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int sg = 0; sg < FSTAGES && cb + sg < fe; ++sg) issue(cb + sg, sg);
+  }
+  __syncwarp();
   const float4 lbp = *reinterpret_cast<const float4*>(p.lb_par);
   unsigned long long nskip = 0;
+  int st = 0;            // ring stage of the next staged region, and its use parity
+  unsigned phase = 0;
   for (int64_t c = cb; c < ce; ++c) {
-    const int64_t reg = c * (FCHUNK / WREG) + warp;
-    const int64_t e0 = reg * WREG + (int64_t)lane * FPER;  // my first entry
+    const int reg = (int)c * (FCHUNK / WREG) + warp;   // m < 2^31: 32-bit entry math
+    const int rbase = reg * WREG + 2 * lane;
     int a[FPER], q[FPER];
     float ub[FPER], lb[FPER];
-    if (p.list == nullptr && e0 + FPER <= p.m) {
-      const int4* ap = reinterpret_cast<const int4*>(p.a + e0);
-      const int4 a0 = ap[0], a1 = ap[1];
-      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
-      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
-      const float4* bp = reinterpret_cast<const float4*>(p.ublb + 2 * e0);
+    const bool staged = c < fe;
+    int nvalid = FPER;
+    if (staged) {
+      mbar_wait(&s_bar[warp][st], phase);
+      const unsigned char* base = wsm + (size_t)st * FREG_BYTES;
+      const int2* as = reinterpret_cast<const int2*>(base);
+      const float4* bs = reinterpret_cast<const float4*>(base + WREG * 4);
 #pragma unroll
       for (int h = 0; h < FPER / 2; ++h) {
-        const float4 v = bp[h];
-        ub[2 * h] = v.x; lb[2 * h] = v.y;
-        ub[2 * h + 1] = v.z; lb[2 * h + 1] = v.w;
+        const int2 av = as[h * 32 + lane];
+        const float4 bv = bs[h * 32 + lane];
+        a[2 * h] = av.x; a[2 * h + 1] = av.y;
+        ub[2 * h] = bv.x; lb[2 * h] = bv.y;
+        ub[2 * h + 1] = bv.z; lb[2 * h + 1] = bv.w;
+        q[2 * h] = rbase + 64 * h;
+        q[2 * h + 1] = rbase + 64 * h + 1;
       }
-#pragma unroll
-      for (int e = 0; e < FPER; ++e) q[e] = (int)(e0 + e);
+      __syncwarp();   // the stage is consumed: refill it
+      if (lane == 0 && c + FSTAGES < fe) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(c + FSTAGES, st);
+      }
+      if (++st == FSTAGES) {
+        st = 0;
+        phase ^= 1u;
+      }
     } else {
+      nvalid = 0;
 #pragma unroll
       for (int e = 0; e < FPER; ++e) {
-        const int64_t li = e0 + e;
-        q[e] = li < p.m ? (p.list ? p.list[li] : (int)li) : -1;
+        const int li = rbase + 64 * (e >> 1) + (e & 1);
+        q[e] = li < p.m ? (p.list ? p.list[li] : li) : -1;
+        nvalid += q[e] >= 0;
         a[e] = q[e] >= 0 ? p.a[q[e]] : -1;
         const float2 v = q[e] >= 0 ? reinterpret_cast<const float2*>(p.ublb)[q[e]]
                                    : make_float2(0.f, 0.f);
@@ -176,74 +289,72 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
         lb[e] = v.y;
       }
     }
+    // skip test + run-length block weights of the kept points (at most two runs per
+    // lane are held; a third, which needs three blocks among 8 entries, goes to
+    // global memory directly)
     unsigned need = 0;
-    int run_a = -1;
-    long long run_w = 0;
-    bool broke = false;
-    int ea = -1;          // cluster whose bound parameters E holds (runs share them)
+    int run_a = -1, run2_a = -1;
+    RunW run_w = 0, run2_w = 0;
+    int ea = -1;          // block whose bound parameters E holds (runs share them)
     float4 E = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int e = 0; e < FPER; ++e) {
-      if (q[e] < 0) continue;
-      bool skip = false;
+      const bool valid = staged || q[e] >= 0;
       const int ae = a[e];
-      if (ae >= 0) {
-        if (ae != ea) {
-          E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
-          ea = ae;
+      if (ae >= 0 && ae != ea) {
+        E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
+        ea = ae;
+      }
+      // lb_evalf without its k == 1 test: A > 0 maps lb~ = inf to inf as well
+      const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
+      const bool skip = valid && ae >= 0 && ub_evalf(E, ub[e]) < lbv;
+      need |= (unsigned)(valid && !skip) << e;
+      if (skip) {
+        const RunW v = (RunW)weight_units<WM>(p.w, q[e], wshift);
+        if (ae == run_a) {
+          run_w += v;
+        } else {
+          if (run_a >= 0) {
+            if (run2_a >= 0)
+              atomicAdd((unsigned long long*)&p.block_w[run2_a], (unsigned long long)run2_w);
+            run2_a = run_a;
+            run2_w = run_w;
+          }
+          run_a = ae;
+          run_w = v;
         }
-        skip = ub_evalf(E, ub[e]) < lb_evalf(lbp.x, lb[e], lbp.y);
-      }
-      if (!skip) {
-        need |= 1u << e;
-        continue;
-      }
-      ++nskip;
-      const long long v = weight_units<WM>(p.w, q[e], wshift);
-      if (ae == run_a) {
-        run_w += v;
-      } else {
-        if (run_a >= 0) {
-          cache_add(s_ckey, s_cval, p.block_w, run_a, run_w);
-          broke = true;
-        }
-        run_a = ae;
-        run_w = v;
       }
     }
-    const unsigned grp = __match_any_sync(FULL, run_a);
-    if (grp == FULL && !__any_sync(FULL, broke) && run_a >= 0) {
-      long long g = run_w;
-      for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(FULL, g, o);
-      if (lane == 0) cache_add(s_ckey, s_cval, p.block_w, run_a, g);
-    } else if (run_a >= 0) {
-      cache_add(s_ckey, s_cval, p.block_w, run_a, run_w);
-    }
-    // warp compaction of the points to scan into the region's own slots
-    const int mine = __popc(need);
-    int incl = mine;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += t;
-    }
-    int off = incl - mine;
-    int32_t* dst = scan + reg * WREG;
-    int32_t* dsa = olda + reg * WREG;
+    nskip += nvalid - __popc(need);
+    tab_add(tab, p.block_w, lane, run2_a >= 0, run2_a, run2_w);
+    tab_add(tab, p.block_w, lane, run_a >= 0, run_a, run_w);
+    // compaction of the points to scan into the region's own slots, in entry order
+    // (entry 64h + 2l + b: ranks from two ballots per h)
+    int32_t* dst = scan + (int64_t)reg * WREG;
+    int32_t* dsa = olda + (int64_t)reg * WREG;
+    const unsigned lt = (1u << lane) - 1;
+    int base = 0;
 #pragma unroll
-    for (int e = 0; e < FPER; ++e)
-      if (need & (1u << e)) {
-        dst[off] = q[e];
-        dsa[off] = a[e];  // the scan writes a only when the block changes
+    for (int h = 0; h < FPER / 2; ++h) {
+      const bool n0 = need & (1u << (2 * h)), n1 = need & (1u << (2 * h + 1));
+      const unsigned b0 = __ballot_sync(FULL, n0), b1 = __ballot_sync(FULL, n1);
+      int off = base + __popc(b0 & lt) + __popc(b1 & lt);
+      if (n0) {
+        dst[off] = q[2 * h];
+        dsa[off] = a[2 * h];  // the scan writes a only when the block changes
         ++off;
       }
-    if (lane == 31) runs[reg] = incl;
+      if (n1) {
+        dst[off] = q[2 * h + 1];
+        dsa[off] = a[2 * h + 1];
+      }
+      base += __popc(b0) + __popc(b1);
+    }
+    if (lane == 0) runs[reg] = base;
   }
   for (int o = 16; o; o >>= 1) nskip += __shfl_xor_sync(FULL, nskip, o);
   if (lane == 0 && nskip) atomicAdd(&p.counters[0], nskip);
-  __syncthreads();
-  for (int i = tid; i < HSLOTS; i += FTH)
-    if (s_ckey[i] >= 0 && s_cval[i] != 0)
-      atomicAdd((unsigned long long*)&p.block_w[s_ckey[i]], (unsigned long long)s_cval[i]);
+  tab_flush(tab, p.block_w, lane);
 }
 
 // -------------------------------------------------------------- scan kernel
@@ -410,16 +521,13 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
                                                    const int32_t* __restrict__ runs,
                                                    unsigned long long* __restrict__ sched,
                                                    int uch) {
+  typedef typename std::conditional<WM == GP_W_UNIT, int, long long>::type RunW;
   __shared__ WarpCand<D> WCs[STH / 32];
-  __shared__ int s_ckey[HSLOTS];
-  __shared__ long long s_cval[HSLOTS];
+  __shared__ WarpTab s_tab[STH / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   WarpCand<D>& W = WCs[warp];
-  for (int i = tid; i < HSLOTS; i += STH) {
-    s_ckey[i] = -1;
-    s_cval[i] = 0;
-  }
-  __syncthreads();
+  WarpTab& tab = s_tab[warp];
+  tab_init(tab, lane);
   unsigned long long nq = 0, nexact = 0;
   const int64_t nunits = (nregions + sreg - 1) / sreg;
   // dynamic schedule: warps take chunks of UCH consecutive units from a counter (the
@@ -582,20 +690,24 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       // too many candidates for the staged set (sparse warm-up samples): every lane
       // walks the center grid around its own point, ring by ring, until the ring's
       // lower bound exceeds its runner-up
-      for (int v = lane; v < total_pts; v += 32) {
-        const int q = pos_of(v);
-        double x[D];
-        load_point<D>(p.X, p.ldx, q, x);
-        int bi;
-        float bestf, secondf;
-        unsigned long long nn = 0;
-        grid_point<D>(p, x, bi, bestf, secondf, nn);
-        nq += nn;
-        if (olda[slot_of(v)] != bi) p.a[q] = bi;
-        store_bounds(p, q, bi, bestf, secondf);
-        cache_add(s_ckey, s_cval, p.block_w, bi, weight_units<WM>(p.w, q, wshift));
+      for (int vb = 0; vb < total_pts; vb += 32) {
+        const int v = vb + lane;
+        const bool valid = v < total_pts;
+        int bi = -1, q = 0;
+        if (valid) {
+          q = pos_of(v);
+          double x[D];
+          load_point<D>(p.X, p.ldx, q, x);
+          float bestf, secondf;
+          unsigned long long nn = 0;
+          grid_point<D>(p, x, bi, bestf, secondf, nn);
+          nq += nn;
+          if (olda[slot_of(v)] != bi) p.a[q] = bi;
+          store_bounds(p, q, bi, bestf, secondf);
+        }
+        tab_add(tab, p.block_w, lane, valid, bi,
+                valid ? (RunW)weight_units<WM>(p.w, q, wshift) : (RunW)0);
       }
-      __syncwarp();
       continue;
     }
     // ---- scan, one point per lane per pass
@@ -694,25 +806,15 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
         secondf = __double2float_rd(second);
       }
       // ---- write back + block weights of the scanned points
-      long long wv = 0;
+      RunW wv = 0;
       int c = -1;
       if (valid) {
         c = bi;
         if (oa != c) p.a[q] = c;   // most rescans keep their block
         store_bounds(p, q, c, bestf, secondf);
-        wv = weight_units<WM>(p.w, q, wshift);
+        wv = (RunW)weight_units<WM>(p.w, q, wshift);
       }
-      const unsigned grp = __match_any_sync(FULL, c);
-      if (WM == GP_W_UNIT) {
-        // one shared-memory add per block present in the pass
-        if (valid && lane == __ffs(grp) - 1) cache_add(s_ckey, s_cval, p.block_w, c, __popc(grp));
-      } else if (grp == FULL && valid) {
-        long long g = wv;
-        for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(FULL, g, o);
-        if (lane == 0) cache_add(s_ckey, s_cval, p.block_w, c, g);
-      } else if (valid) {
-        cache_add(s_ckey, s_cval, p.block_w, c, wv);
-      }
+      tab_add(tab, p.block_w, lane, valid, c, wv);
     }
     __syncwarp();
   }
@@ -722,10 +824,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
   }
   if (lane == 0 && nq) atomicAdd(&p.counters[2], nq);
   if ((p.flags & 1) && lane == 0) atomicAdd(&g_scan_stats[5], nexact);
-  __syncthreads();
-  for (int i = tid; i < HSLOTS; i += STH)
-    if (s_ckey[i] >= 0 && s_cval[i] != 0)
-      atomicAdd((unsigned long long*)&p.block_w[s_ckey[i]], (unsigned long long)s_cval[i]);
+  tab_flush(tab, p.block_w, lane);
 }
 
 // ------------------------------------------------------------------ audit
@@ -1004,11 +1103,11 @@ static int validate(const gp_assign_args* a) {
   return GP_OK;
 }
 
-static unsigned persistent_grid(const void* fn, int threads, int64_t work) {
+static unsigned persistent_grid(const void* fn, int threads, int64_t work, size_t dsmem = 0) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, dsmem);
   int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (work < g) g = work;
   return (unsigned)(g < 1 ? 1 : g);
@@ -1020,8 +1119,14 @@ template <int WM>
 static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout& L,
                          int32_t* scan, int32_t* olda, int32_t* runs,
                          unsigned long long* sched, cudaStream_t s) {
-  unsigned gf = persistent_grid((const void*)filter_kernel<WM>, FTH, L.nchunks);
-  filter_kernel<WM><<<gf, FTH, 0, s>>>(*a, wshift, L.nchunks, scan, olda, runs, sched);
+  static bool attr_set[3] = {false, false, false};
+  const size_t fsm = (size_t)(FTH / 32) * FSTAGES * FREG_BYTES;
+  if (!attr_set[WM]) {
+    cudaFuncSetAttribute(filter_kernel<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    attr_set[WM] = true;
+  }
+  unsigned gf = persistent_grid((const void*)filter_kernel<WM>, FTH, L.nchunks, fsm);
+  filter_kernel<WM><<<gf, FTH, fsm, s>>>(*a, wshift, L.nchunks, scan, olda, runs, sched);
   if (g_sreg == 0) {
     const char* e = getenv("GP_SCAN_REGIONS");
     g_sreg = e ? atoi(e) : -1;
