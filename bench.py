@@ -332,6 +332,7 @@ def run_b200(args):
                 lab, st2 = partition_distributed(pts, w, settings, device=dev)
                 lab_h = lab.cpu()
             else:
+                part = None   # the previous result is consumed: its pinned buffer is reused
                 part, st2 = balanced_kmeans_points(pts, w, settings, return_stats=True)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0

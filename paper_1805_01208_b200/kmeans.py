@@ -308,10 +308,6 @@ class DevicePartitioner:
             self.active_cnt = torch.empty(1, dtype=torch.int64, device=dev)
             del rank_d
         del pts, w
-        if n >= (1 << 26):
-            # hand the bootstrap's transient buffers (sort, permutation) back so the
-            # main loop's workspaces do not fragment around them
-            torch.cuda.empty_cache()
         return self
 
     # ------------------------------------------------------------ helpers
