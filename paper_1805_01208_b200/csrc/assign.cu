@@ -17,6 +17,8 @@
 //            tie-break, write-back, block weights of the scanned points.
 // The result per point is the lowest-index argmin of the reference's
 // effective distance, bit for bit; pruning only decides what is evaluated.
+#include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 #include <type_traits>
 
@@ -520,7 +522,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
                                                    const int32_t* __restrict__ olda,
                                                    const int32_t* __restrict__ runs,
                                                    unsigned long long* __restrict__ sched,
-                                                   int uch) {
+                                                   int uch, int pshift) {
   typedef typename std::conditional<WM == GP_W_UNIT, int, long long>::type RunW;
   __shared__ WarpCand<D> WCs[STH / 32];
   __shared__ WarpTab s_tab[STH / 32];
@@ -537,23 +539,31 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
     if (lane == 0) c = atomicAdd(sched, 1ull);
     return (int64_t)__shfl_sync(FULL, c, 0) * uch;
   };
-  int64_t unit = grab(), next_chunk = grab();
-  // counts of the unit's regions (lane r < sreg holds region r's), prefetched one unit ahead
-  int my_cnt = (unit < nunits && lane < sreg && unit * sreg + lane < nregions)
-                   ? runs[unit * sreg + lane] : 0;
+  // work items: unit u, passes sub, sub + 2^pshift, ... (pshift > 0 spreads the passes
+  // of a small round's few units over more warps)
+  const int64_t nitems = nunits << pshift;
+  const int pstride = 32 << pshift;
+  int64_t item = grab(), next_chunk = grab();
+  // counts of the unit's regions (lane r < sreg holds region r's), prefetched one item ahead
+  auto counts_of = [&](int64_t it) {
+    const int64_t u = it >> pshift;
+    return (it < nitems && lane < sreg && u * sreg + lane < nregions) ? runs[u * sreg + lane] : 0;
+  };
+  int my_cnt = counts_of(item);
   int64_t cur_g = -1;          // group whose candidate list src / nsrc hold
   const int32_t* src = nullptr;
   int nsrc = p.k;
-  for (int64_t nxt; unit < nunits; unit = nxt) {
+  for (int64_t nxt; item < nitems; item = nxt) {
     const int cnt_here = my_cnt;
-    if ((unit + 1) % uch != 0 && unit + 1 < nunits) {
-      nxt = unit + 1;
+    const int64_t unit = item >> pshift;
+    const int p0 = (int)(item & ((1 << pshift) - 1)) * 32;   // first pass of this item
+    if ((item + 1) % uch != 0 && item + 1 < nitems) {
+      nxt = item + 1;
     } else {
       nxt = next_chunk;
-      if (nxt < nunits) next_chunk = grab();
+      if (nxt < nitems) next_chunk = grab();
     }
-    my_cnt = (nxt < nunits && lane < sreg && nxt * sreg + lane < nregions)
-                 ? runs[nxt * sreg + lane] : 0;
+    my_cnt = counts_of(nxt);
     // prefix over the SREG region counts (lanes 0..SREG-1)
     int incl = cnt_here;
 #pragma unroll
@@ -562,7 +572,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       if (lane >= o) incl += t;
     }
     const int total_pts = __shfl_sync(FULL, incl, sreg - 1);
-    if (total_pts == 0) continue;
+    if (total_pts <= p0) continue;
     int rbeg[SREG];
 #pragma unroll
     for (int r = 0; r < SREG; ++r) rbeg[r] = __shfl_sync(FULL, incl - cnt_here, r);
@@ -580,8 +590,8 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
     auto pos_of = [&](int v) { return scan[slot_of(v)]; };
     // software pipeline of the passes: positions two passes ahead, coordinates one
     // pass ahead; the first pass's loads overlap the candidate selection below
-    int qA = lane < total_pts ? pos_of(lane) : 0;
-    int qB = 32 + lane < total_pts ? pos_of(32 + lane) : 0;
+    int qA = p0 + lane < total_pts ? pos_of(p0 + lane) : 0;
+    int qB = p0 + pstride + lane < total_pts ? pos_of(p0 + pstride + lane) : 0;
     // candidate source: the group's hierarchical list, or all k centers
     if (p.group_list) {
       const int64_t g = (unit * sreg * WREG) >> p.group_shift;
@@ -690,7 +700,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       // too many candidates for the staged set (sparse warm-up samples): every lane
       // walks the center grid around its own point, ring by ring, until the ring's
       // lower bound exceeds its runner-up
-      for (int vb = 0; vb < total_pts; vb += 32) {
+      for (int vb = p0; vb < total_pts; vb += pstride) {
         const int v = vb + lane;
         const bool valid = v < total_pts;
         int bi = -1, q = 0;
@@ -711,7 +721,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       continue;
     }
     // ---- scan, one point per lane per pass
-    for (int pb = 0; pb < total_pts; pb += 32) {
+    for (int pb = p0; pb < total_pts; pb += pstride) {
       const int v = pb + lane;
       const bool valid = v < total_pts;
       const int q = valid ? qA : 0;
@@ -719,10 +729,10 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       double x[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) x[j] = xA[j];
-      if (pb + 32 < total_pts) {
+      if (pb + pstride < total_pts) {
         qA = qB;
         load_point<D>(p.X, p.ldx, qA, xA);
-        qB = pb + 64 + lane < total_pts ? pos_of(pb + 64 + lane) : 0;
+        qB = pb + 2 * pstride + lane < total_pts ? pos_of(pb + 2 * pstride + lane) : 0;
       }
       // single pass: the two smallest q = d^2/infl^2 with their slots, and the third value
       double q1 = INFINITY, q2 = INFINITY, q3 = INFINITY;
@@ -1135,20 +1145,31 @@ static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout
   int sreg = g_sreg > 0 ? g_sreg
                        : (a->scan_regions > 0 ? a->scan_regions : (a->list ? 1 : SREG));
   if (sreg > SREG) sreg = SREG;
-  const int64_t wgroups = (L.nregions + sreg * (STH / 32) - 1) / (sreg * (STH / 32));
   // consecutive units per claim only when there are many more units than warps (few,
   // heavy units of a small warm-up sample go one per warp)
   const int64_t nunits = (L.nregions + sreg - 1) / sreg;
+  // and a small round's units split into per-pass items, so more warps share them
+  auto plan = [&](const void* fn, unsigned& gs, int& uch, int& pshift) {
+    const unsigned gmax = persistent_grid(fn, STH, INT64_MAX);
+    const int64_t warps = (int64_t)gmax * (STH / 32);
+    int pmax = 0;
+    while ((1 << (pmax + 1)) <= 8 * sreg) ++pmax;   // a unit has at most 8 * sreg passes
+    pshift = 0;
+    while (pshift < pmax && (nunits << (pshift + 1)) <= 2 * warps) ++pshift;
+    uch = nunits >= 16 * warps ? UCH : 1;
+    const int64_t items = ((nunits << pshift) + (STH / 32) - 1) / (STH / 32);
+    gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>(gmax, items));
+  };
+  unsigned gs;
+  int uch, pshift;
   if (a->d == 2) {
-    unsigned gs = persistent_grid((const void*)scan_kernel<2, WM>, STH, wgroups);
-    const int uch = nunits >= 16ll * gs * (STH / 32) ? UCH : 1;
+    plan((const void*)scan_kernel<2, WM>, gs, uch, pshift);
     scan_kernel<2, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs, sched,
-                                          uch);
+                                          uch, pshift);
   } else {
-    unsigned gs = persistent_grid((const void*)scan_kernel<3, WM>, STH, wgroups);
-    const int uch = nunits >= 16ll * gs * (STH / 32) ? UCH : 1;
+    plan((const void*)scan_kernel<3, WM>, gs, uch, pshift);
     scan_kernel<3, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs, sched,
-                                          uch);
+                                          uch, pshift);
   }
 }
 
