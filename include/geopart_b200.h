@@ -181,6 +181,11 @@ typedef struct gp_assign_args {
   const double* unit_boxes;
   int32_t unit_shift;
   int32_t flags;          /* bit 0: accumulate scan statistics (gp_scan_stats) */
+  /* region-local lower-bound maps (gp_region_maps): entry li uses the float4
+   * lb_rpar[li >> lb_rshift] instead of lb_par; NULL: the global lb_par */
+  const float* lb_rpar;
+  int32_t lb_rshift;
+  int32_t pad2;
 } gp_assign_args;
 int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);
@@ -217,6 +222,21 @@ int gp_update_maps(const double* old_infl, const double* new_infl, const double*
                    double* state, double* inv2_lo, double* inv2_hi, float* ub_eval,
                    float* ub_norm, float* lb_par, int32_t* flags, int reset, double scale_hint,
                    void* stream);
+
+/* Region-local lower-bound maps (full phase, B200 extension of kmeans.py:229-236).
+ * The reference relaxes every lower bound by the smallest influence ratio and the
+ * largest center shift over all k centers.  For the entries of super group r only
+ * the centers of its candidate list (gp_group_candidates, under the NEW centers
+ * and influences) can be the nearest or the runner-up: every other center is
+ * farther than the group's second-smallest upper bound, which bounds the
+ * runner-up of every entry.  So the relaxation over the list alone is sound.
+ * rstate: nregions x 3 doubles (A, B, steps); rpar: nregions x float4 in the
+ * layout of lb_par.  reset = 1: identity maps.  flags[0] = 1 when a map leaves
+ * the float32 range (the caller rebases). */
+int gp_region_maps(const double* old_infl, const double* new_infl, const double* moves, int k,
+                   const int32_t* group_list, const int32_t* group_count, int group_cap,
+                   int64_t nregions, double* rstate, float* rpar, int32_t* flags, int reset,
+                   double scale_hint, void* stream);
 
 /* Re-express every bound under identity maps (when the host's cumulative
  * maps drift out of range).  Same bound semantics as gp_assign_args. */

@@ -34,6 +34,7 @@ class AssignArgs(C.Structure):
         ("workspace", vp), ("workspace_bytes", sz), ("scan_regions", i32), ("grid_n", i32),
         ("grid_start", vp), ("grid_items", vp), ("grid_lo", f64 * 3), ("grid_h", f64),
         ("inv2_min", f64), ("unit_boxes", vp), ("unit_shift", i32), ("flags", i32),
+        ("lb_rpar", vp), ("lb_rshift", i32), ("pad2", i32),
     ]
 
 
@@ -75,6 +76,8 @@ _SIGS = {
     "gp_fold_workspace_bytes": (C.c_int, [i64, i64, i64, C.c_int, C.POINTER(sz)]),
     "gp_movement_fold": (C.c_int, [C.POINTER(FoldArgs), vp]),
     "gp_fold_stats": (C.c_int, [vp]),
+    "gp_region_maps": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, C.c_int, i64, vp, vp, vp, C.c_int,
+                                 f64, vp]),
     "gp_scan_stats": (C.c_int, [vp, C.c_int]),
     "gp_fold_export": (C.c_int, [C.POINTER(FoldArgs), vp, vp, vp, vp]),
     "gp_fold_combine_bytes": (C.c_int, [C.c_int, C.POINTER(sz)]),
@@ -123,7 +126,7 @@ KERNELS_PER_CALL = {
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 3,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
-    "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
+    "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 1, "gp_region_maps": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
 }
 _launches = [0]
 calls: dict[str, int] = {}   # API calls by name (tools/kprof.py)

@@ -60,11 +60,17 @@ __device__ __forceinline__ void box_bounds_sq(const double* c, const double* lo,
 
 // fresh best / runner-up effective distances (b rounded up, s rounded down)
 // -> normalised float32 bounds under the current maps
-__device__ __forceinline__ void store_bounds(const gp_assign_args& p, int64_t q, int c, float b_up,
-                                             float s_dn) {
+__device__ __forceinline__ void store_bounds(const gp_assign_args& p, const float4& L, int64_t q,
+                                             int c, float b_up, float s_dn) {
   const float4 N = reinterpret_cast<const float4*>(p.ub_norm)[c];
-  reinterpret_cast<float2*>(p.ublb)[q] =
-      make_float2(ub_normf(N, b_up), lb_normf(p.lb_par[2], p.lb_par[3], s_dn));
+  reinterpret_cast<float2*>(p.ublb)[q] = make_float2(ub_normf(N, b_up), lb_normf(L.z, L.w, s_dn));
+}
+
+// lower-bound map parameters (A_lo, B_hi, 1/A_lo, B_lo) of active entry li: its
+// region's (gp_region_maps) or the global ones
+__device__ __forceinline__ float4 lb_params(const gp_assign_args& p, int64_t li) {
+  if (p.lb_rpar) return reinterpret_cast<const float4*>(p.lb_rpar)[li >> p.lb_rshift];
+  return *reinterpret_cast<const float4*>(p.lb_par);
 }
 
 // Per-warp block-weight table (no atomics, no cross-warp contention): the lanes'
@@ -242,13 +248,13 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
     for (int sg = 0; sg < FSTAGES && cb + sg < fe; ++sg) issue(cb + sg, sg);
   }
   __syncwarp();
-  const float4 lbp = *reinterpret_cast<const float4*>(p.lb_par);
   unsigned long long nskip = 0;
   int st = 0;            // ring stage of the next staged region, and its use parity
   unsigned phase = 0;
   for (int64_t c = cb; c < ce; ++c) {
     const int reg = (int)c * (FCHUNK / WREG) + warp;   // m < 2^31: 32-bit entry math
     const int rbase = reg * WREG + 2 * lane;
+    const float4 lbp = lb_params(p, (int64_t)reg * WREG);   // one map per 2^15 entries
     int a[FPER], q[FPER];
     float ub[FPER], lb[FPER];
     const bool staged = c < fe;
@@ -602,6 +608,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
         nsrc = gc >= 0 ? gc : p.k;
       }
     }
+    const float4 Lr = lb_params(p, unit * sreg * WREG);
     // ---- box: the unit's static box (all its active entries), or the box of the
     // unit's scanned points
     double lo[D], hi[D];
@@ -713,7 +720,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
           grid_point<D>(p, x, bi, bestf, secondf, nn);
           nq += nn;
           if (olda[slot_of(v)] != bi) p.a[q] = bi;
-          store_bounds(p, q, bi, bestf, secondf);
+          store_bounds(p, Lr, q, bi, bestf, secondf);
         }
         tab_add(tab, p.block_w, lane, valid, bi,
                 valid ? (RunW)weight_units<WM>(p.w, q, wshift) : (RunW)0);
@@ -821,7 +828,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       if (valid) {
         c = bi;
         if (oa != c) p.a[q] = c;   // most rescans keep their block
-        store_bounds(p, q, c, bestf, secondf);
+        store_bounds(p, Lr, q, c, bestf, secondf);
         wv = (RunW)weight_units<WM>(p.w, q, wshift);
       }
       tab_add(tab, p.block_w, lane, valid, c, wv);
@@ -866,7 +873,8 @@ __global__ void audit_kernel(gp_assign_args p, unsigned long long* out) {
     }
     const double ub =
         a >= 0 ? ub_evalf(reinterpret_cast<const float4*>(p.ub_eval)[a], bnd.x) : INFINITY;
-    const double lb = lb_evalf(p.lb_par[0], bnd.y, p.lb_par[1]);
+    const float4 L = lb_params(p, li);
+    const double lb = lb_evalf(L.x, bnd.y, L.y);
     ++aud;
     if (a >= 0 && ub < own) ++viol;
     if (p.k > 1 && lb > m2) ++viol;
@@ -886,7 +894,8 @@ __global__ void rebase_kernel(gp_assign_args p) {
     // the host resets the maps to identity after this pass: store the values themselves
     const float ub = a >= 0 ? ub_evalf(reinterpret_cast<const float4*>(p.ub_eval)[a], bnd.x)
                             : bnd.x;
-    reinterpret_cast<float2*>(p.ublb)[q] = make_float2(ub, lb_evalf(p.lb_par[0], bnd.y, p.lb_par[1]));
+    const float4 L = lb_params(p, li);
+    reinterpret_cast<float2*>(p.ublb)[q] = make_float2(ub, lb_evalf(L.x, bnd.y, L.y));
   }
 }
 
@@ -1102,6 +1111,52 @@ __global__ void __launch_bounds__(1024) update_maps_kernel(
   }
 }
 
+// one warp per region: smallest ratio / largest shift over the region's candidate
+// list (all k when the list overflowed), composed into its lower-bound map like
+// update_maps_kernel composes the global one
+__global__ void __launch_bounds__(256) region_maps_kernel(
+    const double* __restrict__ old_infl, const double* __restrict__ new_infl,
+    const double* __restrict__ moves, int k, const int32_t* __restrict__ glist,
+    const int32_t* __restrict__ gcount, int gcap, int64_t R, double* __restrict__ rst,
+    float4* __restrict__ rpar, int32_t* __restrict__ flags, int reset, double scale_hint) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (r >= R) return;
+  double A = 1.0, B = 0.0, steps = 0.0;
+  if (!reset) {
+    const int gc = gcount[r];
+    const int32_t* lst = gc >= 0 ? glist + r * (int64_t)gcap : nullptr;
+    const int ns = gc >= 0 ? gc : k;
+    double rmin = INFINITY, smax = 0.0;
+    for (int i = lane; i < ns; i += 32) {
+      const int c = lst ? lst[i] : i;
+      rmin = fmin(rmin, old_infl[c] / new_infl[c]);
+      smax = fmax(smax, (moves ? moves[c] : 0.0) / new_infl[c]);
+    }
+    for (int o = 16; o; o >>= 1) {
+      rmin = fmin(rmin, __shfl_xor_sync(FULL, rmin, o));
+      smax = fmax(smax, __shfl_xor_sync(FULL, smax, o));
+    }
+    if (!(rmin < INFINITY)) rmin = 1.0;
+    A = rst[3 * r];
+    B = rst[3 * r + 1];
+    steps = rst[3 * r + 2];
+    A = A * rmin * LBS;
+    B = (B * rmin + smax) * LBS;
+    steps += 1.0;
+  }
+  if (lane == 0) {
+    const double e = (4.0 * steps + 16.0) * 0x1p-52;
+    rst[3 * r] = A;
+    rst[3 * r + 1] = B;
+    rst[3 * r + 2] = steps;
+    rpar[r] = make_float4(__double2float_rd(__dmul_rd(A, 1.0 - e)),
+                          __double2float_ru(__dmul_ru(B, 1.0 + e)),
+                          __double2float_rd(__ddiv_rd(1.0, A)), __double2float_rd(B));
+    if (A < 1e-6 || A > 1e6 || B > 64.0 * scale_hint) flags[0] = 1;
+  }
+}
+
 static int validate(const gp_assign_args* a) {
   GP_REQUIRE(a != nullptr, "null args");
   GP_REQUIRE(a->d == 2 || a->d == 3, "d must be 2 or 3");
@@ -1223,6 +1278,19 @@ int gp_update_maps(const double* old_infl, const double* new_infl, const double*
       old_infl, new_infl, moves, k, state, inv2_lo, inv2_hi, (float4*)ub_eval, (float4*)ub_norm,
       lb_par, flags, reset, scale_hint);
   return check_launch("update_maps");
+}
+
+int gp_region_maps(const double* old_infl, const double* new_infl, const double* moves, int k,
+                   const int32_t* group_list, const int32_t* group_count, int group_cap,
+                   int64_t nregions, double* rstate, float* rpar, int32_t* flags, int reset,
+                   double scale_hint, void* stream) {
+  GP_REQUIRE(k >= 1 && rstate && rpar && flags && nregions >= 1, "gp_region_maps: bad args");
+  GP_REQUIRE(reset || (old_infl && new_infl && group_list && group_count),
+             "gp_region_maps: inputs missing");
+  region_maps_kernel<<<grid_for(nregions * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      old_infl, new_infl, moves, k, group_list, group_count, group_cap, nregions, rstate,
+      (float4*)rpar, flags, reset, scale_hint);
+  return check_launch("region_maps");
 }
 
 int gp_rebase_bounds(const gp_assign_args* args, void* stream) {

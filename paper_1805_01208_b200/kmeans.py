@@ -353,6 +353,8 @@ class DevicePartitioner:
         a.flags = 1 if self.timer is not None and os.environ.get("GP_SCAN_STATS") else 0
         self.aargs = a
         self.hier = _Hierarchy(self, use_mega=k > 4096) if k > 128 else None
+        self.rmaps = None          # region-local lower-bound maps (full phase)
+        self.lists_fresh = False   # candidate lists already match the current parameters
         f = N.FoldArgs()
         f.X, f.ldx, f.d, f.k, f.order3 = self.X.data_ptr(), self.ldx, d, k, self.order3
         f.wmode, f.w, f.a = a.wmode, a.w, self.A.data_ptr()
@@ -387,6 +389,33 @@ class DevicePartitioner:
         self.cur = nxt
         self.aargs.infl = self._infl_ptr(nxt)
         self.aargs.inv2_min = 1.0 / float(np.max(new_infl)) ** 2 * (1.0 - 1e-15)
+        if self.rmaps is not None:
+            self._relax_regions(old, self._infl_ptr(nxt), mv, reset)
+
+    def _enter_region_maps(self, infl):
+        """Full phase with a candidate hierarchy: every super group gets its own
+        lower-bound map (gp_region_maps).  Bounds are materialised under the global
+        maps first, then every map restarts from identity."""
+        a = self.aargs
+        N.count("gp_rebase_bounds")
+        N.check(N.lib.gp_rebase_bounds(C.byref(a), self.sh), "gp_rebase_bounds")
+        self.mapflag.zero_()
+        R = self.hier.ns
+        self.rstate = torch.empty(3 * R, dtype=torch.float64, device=self.device)
+        self.rpar = torch.empty(4 * R, dtype=torch.float32, device=self.device)
+        self.rmaps = R
+        self._set_influence(infl, reset=True)
+        a.lb_rpar, a.lb_rshift = self.rpar.data_ptr(), self.hier.SUPER_SHIFT
+
+    def _relax_regions(self, old_ptr, new_ptr, moves_ptr, reset):
+        h = self.hier
+        if not reset:
+            h.refresh()                # the lists under the new centers and influences
+            self.lists_fresh = True
+        N.call("gp_region_maps", old_ptr, new_ptr, moves_ptr, self.settings.k,
+               h.slist.data_ptr(), h.scount.data_ptr(), h.SUPER_CAP, self.rmaps,
+               self.rstate.data_ptr(), self.rpar.data_ptr(), self.mapflag.data_ptr(),
+               1 if reset else 0, self.scale_hint, self.sh)
 
     def _build_grid(self, centers: np.ndarray):
         """Uniform grid over the point box holding the centers (k-sized host numpy),
@@ -491,8 +520,9 @@ class DevicePartitioner:
         return m
 
     def _assign(self):
-        if self.hier is not None:
+        if self.hier is not None and not self.lists_fresh:
             self.hier.refresh()
+        self.lists_fresh = False
         self.red.zero_()
         if self.timer is not None:
             e0 = self.timer.mark(self.stream)
@@ -567,6 +597,8 @@ class DevicePartitioner:
         for step, (phase, size) in enumerate(plan):
             m = self._set_active(size)
             self.m_global = self._global_count(m)
+            if phase == "full" and self.hier is not None and self.rmaps is None:
+                self._enter_region_maps(infl)
             # ---------------- assign_and_balance (kmeans.py:377-453)
             skips = decisions = evals = 0
             final_imb = math.inf
@@ -684,7 +716,7 @@ class DevicePartitioner:
         """Drop every n-sized device buffer (the caller keeps only the result)."""
         for name in ("X", "W", "A", "A_fb", "UBLB", "A_d", "UBLB_d", "X_d", "W_d", "gids", "rank_sfc", "active_idx",
                      "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier", "grid_start",
-                     "grid_items", "ubox"):
+                     "grid_items", "ubox", "rstate", "rpar"):
             if hasattr(self, name):
                 setattr(self, name, None)
 

@@ -203,6 +203,22 @@ def test_bound_audit_zero_violations():
     assert total >= 1_000_000 and viol == 0 and badskip == 0
 
 
+def test_bound_audit_region_maps():
+    """ACCEPT-04 with the candidate hierarchy (k > 128): the full phase runs on
+    region-local lower-bound maps (gp_region_maps); every bound must still hold."""
+    total = viol = badskip = 0
+    for dim, k, n, seed in ((2, 256, 150_000, 3), (3, 192, 100_000, 4)):
+        rng = np.random.default_rng(seed)
+        pts = rng.random((n, dim))
+        _, stats = balanced_kmeans_points(
+            pts, None, KMeansSettings(k=k, seed=seed, max_iter=12, audit_bounds=True),
+            return_stats=True)
+        total += stats.audited_point_iterations
+        viol += stats.bound_violations
+        badskip += stats.skip_check_failures
+    assert total >= 1_000_000 and viol == 0 and badskip == 0
+
+
 def test_pruning_rate():
     """ACCEPT-06 analogue: skip fraction >= 0.5 over the last three iterations."""
     rng = np.random.default_rng(0)
