@@ -415,7 +415,7 @@ __device__ __forceinline__ double qdist(const double* x, const WarpCand<D>& W, i
 __device__ unsigned long long g_scan_stats[8];  // gp_scan_stats (flags bit 0)
 
 constexpr int UCH = 4;             // scan units per scheduler claim (large rounds)
-constexpr int SREG = 4;            // max filter regions per scan unit (runtime sreg <= SREG)
+constexpr int SREG = 32;           // max filter regions per scan unit (runtime sreg <= SREG)
 constexpr double SEP = 1e-12;      // q separation above which no exact evaluation is needed
 constexpr float AP_HI_F = 1.0f + 2.4e-7f;  // margins of the sqrt(q)-derived float bounds
 constexpr float AP_LO_F = 1.0f - 2.4e-7f;
@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
   typedef typename std::conditional<WM == GP_W_UNIT, int, long long>::type RunW;
   __shared__ WarpCand<D> WCs[STH / 32];
   __shared__ WarpTab s_tab[STH / 32];
+  __shared__ int s_rbeg[STH / 32][SREG];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   WarpCand<D>& W = WCs[warp];
   WarpTab& tab = s_tab[warp];
@@ -579,19 +580,20 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
     }
     const int total_pts = __shfl_sync(FULL, incl, sreg - 1);
     if (total_pts <= p0) continue;
-    int rbeg[SREG];
-#pragma unroll
-    for (int r = 0; r < SREG; ++r) rbeg[r] = __shfl_sync(FULL, incl - cnt_here, r);
-    // v-th scanned point of the unit -> position (static register indexing only)
+    // first scanned point of each region of the unit (shared memory, no registers)
+    int* rbeg = s_rbeg[warp];
+    __syncwarp();
+    if (lane < sreg) rbeg[lane] = incl - cnt_here;
+    __syncwarp();
+    // v-th scanned point of the unit -> slot: the last region r with rbeg[r] <= v
     auto slot_of = [&](int v) {
-      int r = 0, rb = 0;
-#pragma unroll
-      for (int t = 1; t < SREG; ++t)
-        if (t < sreg && v >= rbeg[t]) {
-          r = t;
-          rb = rbeg[t];
-        }
-      return (unit * sreg + r) * WREG + (v - rb);
+      int lo = 0, hi = sreg - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rbeg[mid] <= v) lo = mid;
+        else hi = mid - 1;
+      }
+      return (unit * sreg + lo) * WREG + (v - rbeg[lo]);
     };
     auto pos_of = [&](int v) { return scan[slot_of(v)]; };
     // software pipeline of the passes: positions two passes ahead, coordinates one
@@ -1248,7 +1250,8 @@ int gp_assign_round(const gp_assign_args* args, void* stream) {
   GP_REQUIRE(args->workspace && args->workspace_bytes >= L.total,
              "gp_assign_round: workspace too small");
   if (args->group_list)
-    GP_REQUIRE(SREG * WREG <= (1ll << args->group_shift), "group_shift smaller than a scan unit");
+    GP_REQUIRE((int64_t)(args->scan_regions > 0 ? args->scan_regions : SREG) * WREG <= (1ll << args->group_shift),
+               "group_shift smaller than a scan unit");
   if (args->unit_boxes)
     GP_REQUIRE(args->scan_regions >= 1 && (1ll << args->unit_shift) == args->scan_regions * WREG,
                "unit_shift must equal log2(scan_regions * 256)");

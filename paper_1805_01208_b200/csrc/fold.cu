@@ -208,22 +208,25 @@ __global__ void fold_slots(const uint32_t* __restrict__ skey, int32_t* __restric
     slot[skey[pbeg[p]]] = (int32_t)p;
 }
 
-// Pair folds, G = 32 / NC pairs per warp.  Lane g < G owns group g's cursor
-// (pair, sorted run j, entry cur, run end re); each step the whole warp loads
-// up to 32 consecutive entries of every group's current run, computes w*x, w,
-// w*|x-c|^2 (and the max |x-c|^2 for the extent) and stages them in shared
-// memory; then lane (g, col) folds column col of group g in entry order, which
-// is the bincount order of the reference.  A group whose pair ends writes the
-// pair's partials and takes the next pair from the work counter.
-template <int D, int NC>
+// Pair folds, G pairs per warp (G * NC <= 32), B batches of 32 entries per step.
+// Lane g < G owns group g's cursor (pair, sorted run j, entry cur, run end re);
+// each step the whole warp loads up to 32 B consecutive entries of every group's
+// current run (all loads issued together), computes w*x, w, w*|x-c|^2 (and the
+// max |x-c|^2 for the extent) and stages them in shared memory; then lane
+// (g, col) folds column col of group g in entry order, which is the bincount
+// order of the reference.  A group whose pair ends writes the pair's partials and
+// takes the next pair from the work counter.  Many pairs: G = 32 / NC, B = 1 (lane
+// utilisation); few pairs: G = 1, B = 8 (fewer, longer steps on the critical path).
+template <int D, int NC, int G, int B>
 __global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t* __restrict__ starts,
                                                   const int32_t* __restrict__ sidx,
                                                   const uint32_t* __restrict__ skey,
                                                   const int32_t* __restrict__ pbeg,
                                                   int64_t* counters, double* __restrict__ out) {
-  constexpr int G = 32 / NC;
+  static_assert(G * NC <= 32 && G * B <= 32, "fold_groups shape");
   constexpr int W = FT / 32;
-  __shared__ double st[W][G * NC][33];
+  constexpr int T = 32 * B;        // entries per group step
+  __shared__ double st[W][G * NC][T + 1];
   __shared__ double scen[W][G][D];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t P = counters[3];
@@ -255,36 +258,44 @@ __global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t*
   for (int g = 0; g < G; ++g) extg[g] = 0.0;
   for (;;) {
     const bool live = lane < G && pair >= 0;
-    const int cnt = live ? min(32, re - cur) : 0;
+    const int cnt = live ? min(T, re - cur) : 0;
     if (!__any_sync(FULL, live)) break;
     // all groups' loads first (clamped to a valid entry), so they are in flight together
     int ngs[G];
-    double xr[G][D], wr[G];
+    double xr[G][B][D], wr[G][B];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int cg = __shfl_sync(FULL, cur, g);
       ngs[g] = __shfl_sync(FULL, cnt, g);
-      const int i = ngs[g] > 0 ? cg + min(lane, ngs[g] - 1) : 0;
-      wr[g] = load_weight(f.w, f.wmode, i);
-      if (NC > 1) load_point<D>(f.X, f.ldx, i, xr[g]);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int t = b * 32 + lane;
+        const int i = ngs[g] > 0 ? cg + min(t, ngs[g] - 1) : 0;
+        wr[g][b] = load_weight(f.w, f.wmode, i);
+        if (NC > 1) load_point<D>(f.X, f.ldx, i, xr[g][b]);
+      }
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      if (lane < ngs[g]) {
-        const double w = wr[g];
-        if (NC == 1) {
-          st[warp][g][lane] = w;
-        } else {
-          double diff[D];
 #pragma unroll
-          for (int q = 0; q < D; ++q) {
-            st[warp][g * NC + q][lane] = __dmul_rn(xr[g][q], w);  // wx = points * weights[:, None]
-            diff[q] = __dsub_rn(xr[g][q], scen[warp][g][q]);
+      for (int b = 0; b < B; ++b) {
+        const int t = b * 32 + lane;
+        if (t < ngs[g]) {
+          const double w = wr[g][b];
+          if (NC == 1) {
+            st[warp][g][t] = w;
+          } else {
+            double diff[D];
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+              st[warp][g * NC + q][t] = __dmul_rn(xr[g][b][q], w);  // wx = points * weights[:, None]
+              diff[q] = __dsub_rn(xr[g][b][q], scen[warp][g][q]);
+            }
+            const double sq = sqnorm_rn(diff, D, f.order3);
+            st[warp][g * NC + D][t] = w;
+            st[warp][g * NC + D + 1][t] = __dmul_rn(sq, w);
+            extg[g] = fmax(extg[g], sq);  // sqrt is monotone: max of sqrt = sqrt of max
           }
-          const double sq = sqnorm_rn(diff, D, f.order3);
-          st[warp][g * NC + D][lane] = w;
-          st[warp][g * NC + D + 1][lane] = __dmul_rn(sq, w);
-          extg[g] = fmax(extg[g], sq);  // sqrt is monotone: max of sqrt = sqrt of max
         }
       }
     }
@@ -292,9 +303,9 @@ __global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t*
     const int nmine = __shfl_sync(FULL, cnt, mg < G ? mg : 0);
     if (mg < G) {
       const double* colp = st[warp][mg * NC + col];
-      if (nmine == 32) {
-#pragma unroll
-        for (int t = 0; t < 32; ++t) acc = __dadd_rn(acc, colp[t]);
+      if (nmine == T) {
+#pragma unroll 32
+        for (int t = 0; t < T; ++t) acc = __dadd_rn(acc, colp[t]);
       } else {
         for (int t = 0; t < nmine; ++t) acc = __dadd_rn(acc, colp[t]);
       }
@@ -336,6 +347,16 @@ __global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t*
       __syncwarp();
     }
   }
+}
+
+template <int D, int NC, int G, int B>
+static void launch_fold_groups(const gp_fold_args* f, int sms, const int32_t* starts,
+                               const int32_t* sidx, const uint32_t* skey, const int32_t* pbeg,
+                               int64_t* counters, double* out, cudaStream_t s) {
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<D, NC, G, B>, FT, 0);
+  fold_groups<D, NC, G, B><<<sms * (per_sm > 0 ? per_sm : 1), FT, 0, s>>>(
+      *f, starts, sidx, skey, pbeg, counters, out);
 }
 
 // One warp per block: gather the block's pair partials over the segments
@@ -500,6 +521,7 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
 
   GP_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(int64_t), s));
   GP_CUDA(cudaMemsetAsync(slot, 0xff, L.cells * sizeof(int32_t), s));
+  int64_t R_host = 0;
   if (cnt > 0) {
     const int64_t nt = (cnt + RTILE - 1) / RTILE;
     run_count<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, tiles);
@@ -510,6 +532,7 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     int64_t R = 0;
     GP_CUDA(cudaMemcpyAsync(&R, counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     GP_CUDA(cudaStreamSynchronize(s));
+    R_host = R;
     // stable LSD radix sort with ping-pong buffers (no n-sized CUB scratch)
     cub::DoubleBuffer<uint32_t> kb(rkey, skey);
     cub::DoubleBuffer<int32_t> vb(ridx, sidx);
@@ -533,21 +556,24 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
                                        pbeg, counters + 3, (int)R, s));
     fold_slots<<<grid_for(R, 256, sms * 8), 256, 0, s>>>(skey, pbeg, counters, slot);
   }
-  int per_sm = 1;
+  // many pairs: G pairs per warp for lane utilisation; few (long) pairs: one pair
+  // per warp with 256-entry steps.  The pair count is known once the runs are
+  // sorted (read back with R above: P <= R).
+  const bool few = cnt > 0 && R_host < (int64_t)sms * 64;
   if (f->weights_only) {
     if (f->d == 2) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<2, 1>, FT, 0);
-      fold_groups<2, 1><<<sms * per_sm, FT, 0, s>>>(*f, starts, sidx, skey, pbeg, counters, out);
+      if (few) launch_fold_groups<2, 1, 1, 8>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+      else launch_fold_groups<2, 1, 32, 1>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
     } else {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<3, 1>, FT, 0);
-      fold_groups<3, 1><<<sms * per_sm, FT, 0, s>>>(*f, starts, sidx, skey, pbeg, counters, out);
+      if (few) launch_fold_groups<3, 1, 1, 8>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+      else launch_fold_groups<3, 1, 32, 1>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
     }
   } else if (f->d == 2) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<2, 4>, FT, 0);
-    fold_groups<2, 4><<<sms * per_sm, FT, 0, s>>>(*f, starts, sidx, skey, pbeg, counters, out);
+    if (few) launch_fold_groups<2, 4, 1, 8>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+    else launch_fold_groups<2, 4, 8, 1>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
   } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_groups<3, 5>, FT, 0);
-    fold_groups<3, 5><<<sms * per_sm, FT, 0, s>>>(*f, starts, sidx, skey, pbeg, counters, out);
+    if (few) launch_fold_groups<3, 5, 1, 8>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+    else launch_fold_groups<3, 5, 6, 1>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
   }
   if (f->d == 2) fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   else fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);

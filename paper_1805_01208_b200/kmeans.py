@@ -136,21 +136,35 @@ def sample_ranks_device(n: int, seed: int, device, stream) -> torch.Tensor:
     return rank
 
 
+def full_scan_regions(n: int, k: int) -> int:
+    """Full-phase scan unit in 256-entry filter regions: about 1/8 of a block's
+    points (SFC-compact units whose boxes stay small against a block), 1..32."""
+    if os.environ.get("GP_FULL_SREG"):   # tuning override
+        return int(os.environ["GP_FULL_SREG"])
+    target = max(1, n // (8 * k))
+    r = 1
+    while r < 32 and 256 * r * 2 <= target:
+        r *= 2
+    return r
+
+
 class _Hierarchy:
     """Group-level candidate lists (gp_group_boxes / gp_group_candidates).
 
-    Super groups of 2^15 active entries take their candidates from mega groups
+    Super groups of 2^14 active entries take their candidates from mega groups
     of 2^20 entries (k > 4096) or from all k; tiles of the assign kernel then
     start from their super group's list instead of all k centers.
     """
 
-    SUPER_SHIFT, MEGA_SHIFT = 15, 20
+    SUPER_SHIFT, MEGA_SHIFT = 14, 20
     SUPER_CAP, MEGA_CAP = 1024, 4096
 
     def __init__(self, eng, use_mega: bool):
         self.eng = weakref.proxy(eng)  # no engine <-> hierarchy cycle keeping GBs alive
         self.use_mega = use_mega
         self.key = None
+        if os.environ.get("GP_SUPER_SHIFT"):   # tuning override
+            self.SUPER_SHIFT = int(os.environ["GP_SUPER_SHIFT"])
 
     def prepare(self, list_ptr, m):
         """Boxes of the groups of the current active list (once per active set)."""
@@ -509,7 +523,7 @@ class DevicePartitioner:
         a = self.aargs
         if size is None:
             a.list, a.m = None, self.n
-            a.scan_regions = 4   # dense SFC-contiguous entries: 1024-entry scan units
+            a.scan_regions = full_scan_regions(self.n_global, self.settings.k)
             return self.n
         a.scan_regions = 1       # sparse warm-up sample: 256-entry units
         N.call("gp_compact_active", self.rank_sfc.data_ptr(), self.n, size,
