@@ -521,7 +521,6 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
 
   GP_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(int64_t), s));
   GP_CUDA(cudaMemsetAsync(slot, 0xff, L.cells * sizeof(int32_t), s));
-  int64_t R_host = 0;
   if (cnt > 0) {
     const int64_t nt = (cnt + RTILE - 1) / RTILE;
     run_count<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, tiles);
@@ -532,7 +531,6 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     int64_t R = 0;
     GP_CUDA(cudaMemcpyAsync(&R, counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     GP_CUDA(cudaStreamSynchronize(s));
-    R_host = R;
     // stable LSD radix sort with ping-pong buffers (no n-sized CUB scratch)
     cub::DoubleBuffer<uint32_t> kb(rkey, skey);
     cub::DoubleBuffer<int32_t> vb(ridx, sidx);
@@ -556,25 +554,39 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
                                        pbeg, counters + 3, (int)R, s));
     fold_slots<<<grid_for(R, 256, sms * 8), 256, 0, s>>>(skey, pbeg, counters, slot);
   }
-  // many pairs: G pairs per warp for lane utilisation; few (long) pairs: one pair
-  // per warp with 256-entry steps.  The pair count is known once the runs are
-  // sorted (read back with R above: P <= R).
-  const bool few = cnt > 0 && R_host < (int64_t)sms * 64;
+  // pairs per warp G and batches per step B (G * B = 8 register sets): enough groups
+  // to fill every resident warp, and otherwise longer steps for the critical path
+  int64_t P_host = 0;
+  if (cnt > 0) {
+    GP_CUDA(cudaMemcpyAsync(&P_host, counters + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    GP_CUDA(cudaStreamSynchronize(s));
+  }
+  const int64_t warps = (int64_t)sms * 16;   // ~resident fold warps
+  const int64_t per = P_host / warps;        // pairs per warp if every warp is busy
+#define GP_FOLD(Dd, NCc, Gg, Bb) \
+  launch_fold_groups<Dd, NCc, Gg, Bb>(f, sms, starts, sidx, skey, pbeg, counters, out, s)
   if (f->weights_only) {
     if (f->d == 2) {
-      if (few) launch_fold_groups<2, 1, 1, 8>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
-      else launch_fold_groups<2, 1, 32, 1>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+      if (per >= 32) GP_FOLD(2, 1, 32, 1);
+      else if (per >= 4) GP_FOLD(2, 1, 4, 8);
+      else GP_FOLD(2, 1, 1, 8);
     } else {
-      if (few) launch_fold_groups<3, 1, 1, 8>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
-      else launch_fold_groups<3, 1, 32, 1>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+      if (per >= 32) GP_FOLD(3, 1, 32, 1);
+      else if (per >= 4) GP_FOLD(3, 1, 4, 8);
+      else GP_FOLD(3, 1, 1, 8);
     }
   } else if (f->d == 2) {
-    if (few) launch_fold_groups<2, 4, 1, 8>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
-    else launch_fold_groups<2, 4, 8, 1>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+    if (per >= 8) GP_FOLD(2, 4, 8, 1);
+    else if (per >= 4) GP_FOLD(2, 4, 4, 2);
+    else if (per >= 2) GP_FOLD(2, 4, 2, 4);
+    else GP_FOLD(2, 4, 1, 8);
   } else {
-    if (few) launch_fold_groups<3, 5, 1, 8>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
-    else launch_fold_groups<3, 5, 6, 1>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+    if (per >= 6) GP_FOLD(3, 5, 6, 1);
+    else if (per >= 4) GP_FOLD(3, 5, 4, 2);
+    else if (per >= 2) GP_FOLD(3, 5, 2, 4);
+    else GP_FOLD(3, 5, 1, 8);
   }
+#undef GP_FOLD
   if (f->d == 2) fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   else fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
   return check_launch("movement_fold");
