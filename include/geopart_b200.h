@@ -233,6 +233,11 @@ int gp_update_maps(const double* old_infl, const double* new_infl, const double*
  * rstate: nregions x 3 doubles (A, B, steps); rpar: nregions x float4 in the
  * layout of lb_par.  reset = 1: identity maps.  flags[0] = 1 when a map leaves
  * the float32 range (the caller rebases). */
+/* Lower bounds of the active entries between the maps: mode 0 materialises them
+ * under the global map (lb_par; identity region maps follow), mode 1 renormalises
+ * them from the region maps (lb_rpar) to the global map. */
+int gp_lb_remap(const gp_assign_args* args, int mode, void* stream);
+
 int gp_region_maps(const double* old_infl, const double* new_infl, const double* moves, int k,
                    const int32_t* group_list, const int32_t* group_count, int group_cap,
                    int64_t nregions, double* rstate, float* rpar, int32_t* flags, int reset,

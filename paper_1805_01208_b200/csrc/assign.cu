@@ -887,6 +887,25 @@ __global__ void audit_kernel(gp_assign_args p, unsigned long long* out) {
   atomicAdd(&out[2], bad);
 }
 
+// lower bounds of the active entries between the global map and region maps:
+// mode 0: materialise under the global map (identity region maps follow);
+// mode 1: region maps -> normalised under the global map again
+__global__ void lb_remap_kernel(gp_assign_args p, int mode) {
+  for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < p.m;
+       li += (int64_t)gridDim.x * blockDim.x) {
+    const int q = p.list ? p.list[li] : (int)li;
+    float2 bnd = reinterpret_cast<const float2*>(p.ublb)[q];
+    const float4 G = *reinterpret_cast<const float4*>(p.lb_par);
+    if (mode == 0) {
+      bnd.y = lb_evalf(G.x, bnd.y, G.y);
+    } else {
+      const float4 L = reinterpret_cast<const float4*>(p.lb_rpar)[li >> p.lb_rshift];
+      bnd.y = lb_normf(G.z, G.w, lb_evalf(L.x, bnd.y, L.y));
+    }
+    reinterpret_cast<float2*>(p.ublb)[q] = bnd;
+  }
+}
+
 __global__ void rebase_kernel(gp_assign_args p) {
   for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < p.m;
        li += (int64_t)gridDim.x * blockDim.x) {
@@ -1294,6 +1313,15 @@ int gp_region_maps(const double* old_infl, const double* new_infl, const double*
       old_infl, new_infl, moves, k, group_list, group_count, group_cap, nregions, rstate,
       (float4*)rpar, flags, reset, scale_hint);
   return check_launch("region_maps");
+}
+
+int gp_lb_remap(const gp_assign_args* args, int mode, void* stream) {
+  int rc = validate(args);
+  if (rc) return rc;
+  GP_REQUIRE(mode == 0 || (mode == 1 && args->lb_rpar), "gp_lb_remap: bad mode");
+  if (args->m == 0) return GP_OK;
+  lb_remap_kernel<<<grid_for(args->m, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(*args, mode);
+  return check_launch("lb_remap");
 }
 
 int gp_rebase_bounds(const gp_assign_args* args, void* stream) {

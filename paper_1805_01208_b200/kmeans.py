@@ -414,10 +414,7 @@ class DevicePartitioner:
         N.count("gp_rebase_bounds")
         N.check(N.lib.gp_rebase_bounds(C.byref(a), self.sh), "gp_rebase_bounds")
         self.mapflag.zero_()
-        R = self.hier.ns
-        self.rstate = torch.empty(3 * R, dtype=torch.float64, device=self.device)
-        self.rpar = torch.empty(4 * R, dtype=torch.float32, device=self.device)
-        self.rmaps = R
+        self._alloc_region_maps(self.hier.ns)
         self._set_influence(infl, reset=True)
         a.lb_rpar, a.lb_rshift = self.rpar.data_ptr(), self.hier.SUPER_SHIFT
 
@@ -458,12 +455,34 @@ class DevicePartitioner:
     def _set_active(self, size):
         m = self._set_active_list(size)
         # (general-weight mode folds block weights from the full arrays every round)
-        if size is not None and self.wplan.exact:
+        dense = size is not None and self.wplan.exact
+        if dense:
             self._enter_dense(m)
         if self.hier is not None:
             self.hier.prepare(self.aargs.list, m)
         self._unit_boxes(m)
+        if dense and self.hier is not None:
+            self._sample_region_maps()
         return m
+
+    def _alloc_region_maps(self, R):
+        if getattr(self, "rcap", 0) < R:
+            self.rcap = R
+            self.rstate = torch.empty(3 * R, dtype=torch.float64, device=self.device)
+            self.rpar = torch.empty(4 * R, dtype=torch.float32, device=self.device)
+        self.rmaps = R
+
+    def _sample_region_maps(self):
+        """Dense warm-up sample: region-local lower-bound maps over the sample's super
+        groups for this step's balance rounds (lower bounds materialised under the
+        global map on entry, renormalised to it in _leave_dense)."""
+        a = self.aargs
+        N.call("gp_lb_remap", C.byref(a), 0, self.sh)
+        self._alloc_region_maps(self.hier.ns)
+        N.call("gp_region_maps", None, None, None, self.settings.k, None, None, 0, self.rmaps,
+               self.rstate.data_ptr(), self.rpar.data_ptr(), self.mapflag.data_ptr(), 1,
+               self.scale_hint, self.sh)
+        a.lb_rpar, a.lb_rshift = self.rpar.data_ptr(), self.hier.SUPER_SHIFT
 
     def _unit_boxes(self, m):
         """Static box of every scan unit over its active entries (once per active set)."""
@@ -503,6 +522,7 @@ class DevicePartitioner:
         a.X, a.a, a.ublb, a.w = (self.X_d.data_ptr(), self.A_d.data_ptr(),
                                  self.UBLB_d.data_ptr(), _ptr(self.W_d))
         a.list, a.m = None, m
+        a.scan_regions = full_scan_regions(m, self.settings.k)  # dense SFC-ordered entries
         self.dense_m = m
 
     def _leave_dense(self):
@@ -512,6 +532,11 @@ class DevicePartitioner:
             self.fold_dense = None
             return
         self.fold_dense = self.dense_m
+        if self.rmaps is not None:
+            # region maps end with the sample step: back to the global lower-bound map
+            N.call("gp_lb_remap", C.byref(self.aargs), 1, self.sh)
+            self.aargs.lb_rpar = None
+            self.rmaps = None
         N.call("gp_scatter_state", self.active_idx.data_ptr(), self.dense_m, self.A_d.data_ptr(),
                self.UBLB_d.data_ptr(), self.A.data_ptr(), self.UBLB.data_ptr(), self.sh)
         a = self.aargs
