@@ -17,7 +17,9 @@
 //              objective terms (kmeans.py:490-499) are computed in parallel
 //              by all lanes of the chunk;
 //   combine  : per block, fold the pair partials in segment order.
+#include <cub/agent/single_pass_scan_operators.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cuda/std/functional>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -29,6 +31,15 @@ namespace gp {
 
 constexpr int FT = 128;     // threads per fold CTA (4 warps; ~34 KB of staging)
 constexpr int MAXCOL = 5;   // d wx columns + w + objective (d <= 3)
+
+// Pair keys are (local segment << bb) | block with bb = bit length of k, so that the
+// run sort needs only the block bits (runs are in entry order, hence segment order
+// within a block) and the invalid key 0xffffffff still sorts last.
+__host__ __device__ __forceinline__ int block_bits(int k) {
+  int bb = 1;
+  while ((1 << bb) <= k) ++bb;
+  return bb;
+}
 
 // counters[]: 0 runs, 1 work cursor, 2 valid runs, 3 pairs
 struct FoldLayout {
@@ -47,7 +58,7 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   L.s0 = n_local > 0 ? seg(pos0) : 0;
   int64_t s1 = n_local > 0 ? seg(pos0 + n_local - 1) : 0;
   L.nseg = n_local > 0 ? s1 - L.s0 + 1 : 1;
-  L.cells = L.nseg * k;
+  L.cells = L.nseg << block_bits(k);   // key space (segment, block)
   L.cap = n_local > 0 ? n_local : 1;
   L.pcap = L.cells < L.cap ? L.cells : L.cap;  // pairs <= min(segments x blocks, runs)
   L.ntiles = (L.cap + RTILE - 1) / RTILE;
@@ -76,7 +87,9 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   L.off_out = o; o = al(o + L.pcap * (MAXCOL + 1) * sizeof(double));
   L.off_counters = o; o = al(o + 8 * sizeof(int64_t));
   L.off_cub = o; o = al(o + L.cub_bytes);
-  L.off_tiles = o; o = al(o + (L.ntiles + 1) * 4);
+  size_t tsb = 0;
+  cub::ScanTileState<int>::AllocationSize((int)L.ntiles, tsb);
+  L.off_tiles = o; o = al(o + tsb);
   L.total = o;
   return L;
 }
@@ -103,7 +116,7 @@ __device__ __forceinline__ unsigned run_marks(const gp_fold_args& f, int64_t cnt
   int prev = -2;
   if (i0 > 0) {
     const int c = f.a[i0 - 1];
-    prev = c >= 0 ? (int)((seg_at(i0 - 1) - s0) * f.k + c) : -1;
+    prev = c >= 0 ? (int)(((seg_at(i0 - 1) - s0) << block_bits(f.k)) | c) : -1;
   }
   int seg = 0;
   int64_t next_b = 0;
@@ -112,6 +125,7 @@ __device__ __forceinline__ unsigned run_marks(const gp_fold_args& f, int64_t cnt
     next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * f.n_global >> 8) - f.pos0 : INT64_MAX;
   }
   unsigned m = 0;
+  const int bb = block_bits(f.k);
 #pragma unroll
   for (int e = 0; e < RPER; ++e) {
     const int64_t i = i0 + e;
@@ -130,7 +144,7 @@ __device__ __forceinline__ unsigned run_marks(const gp_fold_args& f, int64_t cnt
       }
       sg = seg;
     }
-    const int kk = av[e] >= 0 ? (int)((sg - s0) * f.k + av[e]) : -1;
+    const int kk = av[e] >= 0 ? (int)(((sg - s0) << bb) | av[e]) : -1;
     key[e] = kk;
     if (kk != prev) m |= 1u << e;
     prev = kk;
@@ -138,38 +152,36 @@ __device__ __forceinline__ unsigned run_marks(const gp_fold_args& f, int64_t cnt
   return m;
 }
 
-// pass 1: number of run starts per tile of RTILE entries
-__global__ void __launch_bounds__(RT) run_count(gp_fold_args f, int64_t cnt, int64_t s0,
-                                                int32_t* __restrict__ tiles) {
-  __shared__ int ws[RT / 32];
-  const int64_t i0 = (int64_t)blockIdx.x * RTILE + (int64_t)threadIdx.x * RPER;
-  int32_t key[RPER];
-  int c = i0 < cnt ? __popc(run_marks(f, cnt, s0, i0, key)) : 0;
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < RT / 32; ++w) t += ws[w];
-    tiles[blockIdx.x] = t;
-  }
-}
+typedef cub::ScanTileState<int> RunTiles;
 
-// pass 2: run r (in entry order) -> starts[r] = first entry, (key, r) for the
-// sort; runs with key -1 (unassigned / inactive) sort last
-__global__ void __launch_bounds__(RT) run_write(gp_fold_args f, int64_t cnt, int64_t s0,
-                                                const int32_t* __restrict__ tile_off,
-                                                int64_t ntiles, int32_t* __restrict__ starts,
-                                                uint32_t* __restrict__ rkey,
-                                                int32_t* __restrict__ ridx, int64_t* counters) {
+__global__ void run_tiles_init(RunTiles ts, int ntiles) { ts.InitializeStatus(ntiles); }
+
+// One pass over a: run r (in entry order) -> starts[r] = first entry, (key, r) for
+// the sort; the tile offsets come from a decoupled look-back over the tiles'
+// run counts.  Runs with key -1 (unassigned / inactive) sort last.
+__global__ void __launch_bounds__(RT) run_single(gp_fold_args f, int64_t cnt, int64_t s0,
+                                                 RunTiles ts, int64_t ntiles,
+                                                 int32_t* __restrict__ starts,
+                                                 uint32_t* __restrict__ rkey,
+                                                 int32_t* __restrict__ ridx, int64_t* counters) {
   typedef cub::BlockScan<int, RT> Scan;
+  typedef cub::TilePrefixCallbackOp<int, ::cuda::std::plus<int>, RunTiles> Prefix;
   __shared__ typename Scan::TempStorage tmp;
-  const int64_t i0 = (int64_t)blockIdx.x * RTILE + (int64_t)threadIdx.x * RPER;
+  __shared__ typename Prefix::TempStorage ptmp;
+  const int tile = blockIdx.x;
+  const int64_t i0 = (int64_t)tile * RTILE + (int64_t)threadIdx.x * RPER;
   int32_t key[RPER];
   const unsigned m = i0 < cnt ? run_marks(f, cnt, s0, i0, key) : 0u;
   int excl;
-  Scan(tmp).ExclusiveSum(__popc(m), excl);
-  int r = tile_off[blockIdx.x] + excl;
+  if (tile == 0) {
+    int agg;
+    Scan(tmp).ExclusiveSum(__popc(m), excl, agg);
+    if (threadIdx.x == 0) ts.SetInclusive(0, agg);
+  } else {
+    Prefix op(ts, ptmp, ::cuda::std::plus<int>(), tile);
+    Scan(tmp).ExclusiveSum(__popc(m), excl, op);
+  }
+  int r = excl;
   int valid = 0;
 #pragma unroll
   for (int e = 0; e < RPER; ++e)
@@ -183,10 +195,9 @@ __global__ void __launch_bounds__(RT) run_write(gp_fold_args f, int64_t cnt, int
   for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(FULL, valid, o);
   if ((threadIdx.x & 31) == 0 && valid)
     atomicAdd((unsigned long long*)&counters[2], (unsigned long long)valid);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const int R = tile_off[ntiles];
-    starts[R] = (int32_t)cnt;  // sentinel end
-    counters[0] = R;
+  if (tile == ntiles - 1 && threadIdx.x == RT - 1) {
+    starts[r] = (int32_t)cnt;  // sentinel end (r = total runs)
+    counters[0] = r;
   }
 }
 
@@ -244,7 +255,7 @@ __global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t*
     cur = starts[r];
     re = starts[r + 1];
     if (NC > 1) {
-      const int c = (int)(skey[j] % (uint32_t)f.k);
+      const int c = (int)(skey[j] & ((1u << block_bits(f.k)) - 1));
 #pragma unroll
       for (int q = 0; q < D; ++q) scen[warp][lane][q] = f.centers[c * D + q];
     }
@@ -362,8 +373,10 @@ static void launch_fold_groups(const gp_fold_args* f, int sms, const int32_t* st
 // One warp per block: gather the block's pair partials over the segments
 // (independent loads), then fold them in segment order (np.add.reduce(axis=0)).
 template <int D>
+// slot[] index of (segment s, block c): (s << bb) | c for the local pair keys (bb > 0),
+// s * k + c for the gathered global keys of gp_fold_combine (bb = 0)
 __global__ void fold_combine(gp_fold_args f, const int32_t* __restrict__ slot, int64_t nseg,
-                             const double* __restrict__ out) {
+                             const double* __restrict__ out, int bb) {
   __shared__ int32_t s_slot[4][GP_SEGMENTS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 4 + warp;
@@ -371,7 +384,7 @@ __global__ void fold_combine(gp_fold_args f, const int32_t* __restrict__ slot, i
   int base = 0;
   for (int64_t s0 = 0; s0 < nseg; s0 += 32) {
     int64_t s = s0 + lane;
-    int32_t p = s < nseg ? slot[s * f.k + c] : -1;
+    int32_t p = s < nseg ? slot[bb ? ((s << bb) | c) : s * f.k + c] : -1;
     unsigned m = __ballot_sync(FULL, p >= 0);
     if (p >= 0) s_slot[warp][base + __popc(m & ((1u << lane) - 1))] = p;
     base += __popc(m);
@@ -408,7 +421,8 @@ __global__ void fold_export_kernel(const uint32_t* __restrict__ skey,
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
        p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t key = skey[pbeg[p]];
-    const int64_t seg = key / (uint32_t)k + s0, c = key % (uint32_t)k;
+    const int bb = block_bits(k);
+    const int64_t seg = (key >> bb) + s0, c = key & ((1u << bb) - 1);
     keys[p] = seg * k + c;
 #pragma unroll
     for (int j = 0; j < MAXCOL + 1; ++j) vals[p * (MAXCOL + 1) + j] = out[p * (MAXCOL + 1) + j];
@@ -475,8 +489,8 @@ int gp_fold_combine(const int64_t* keys, const double* vals, int64_t npairs, int
   f.wsum = wsum;
   f.extent = extent;
   f.objective = objective;
-  if (d == 2) fold_combine<2><<<grid_for(k, 4), 128, 0, s>>>(f, slot, GP_SEGMENTS, vals);
-  else fold_combine<3><<<grid_for(k, 4), 128, 0, s>>>(f, slot, GP_SEGMENTS, vals);
+  if (d == 2) fold_combine<2><<<grid_for(k, 4), 128, 0, s>>>(f, slot, GP_SEGMENTS, vals, 0);
+  else fold_combine<3><<<grid_for(k, 4), 128, 0, s>>>(f, slot, GP_SEGMENTS, vals, 0);
   return check_launch("fold_combine");
 }
 
@@ -511,7 +525,6 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
   int32_t* slot = (int32_t*)(ws + L.off_slot);
   double* out = (double*)(ws + L.off_out);
   int64_t* counters = (int64_t*)(ws + L.off_counters);
-  int32_t* tiles = (int32_t*)(ws + L.off_tiles);
   g_last_counters = counters;
   void* cub_tmp = ws + L.off_cub;
   int dev = 0, sms = 148;
@@ -523,23 +536,22 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
   GP_CUDA(cudaMemsetAsync(slot, 0xff, L.cells * sizeof(int32_t), s));
   if (cnt > 0) {
     const int64_t nt = (cnt + RTILE - 1) / RTILE;
-    run_count<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, tiles);
-    GP_CUDA(cudaMemsetAsync(tiles + nt, 0, sizeof(int32_t), s));
-    size_t b = L.cub_bytes;
-    GP_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, b, tiles, tiles, (int)nt + 1, s));
-    run_write<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, tiles, nt, starts, rkey, ridx, counters);
+    RunTiles ts;
+    size_t tsb = 0;
+    RunTiles::AllocationSize((int)nt, tsb);
+    GP_CUDA(ts.Init((int)nt, ws + L.off_tiles, tsb));
+    run_tiles_init<<<grid_for(nt, 256), 256, 0, s>>>(ts, (int)nt);
+    run_single<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, ts, nt, starts, rkey, ridx, counters);
     int64_t R = 0;
     GP_CUDA(cudaMemcpyAsync(&R, counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     GP_CUDA(cudaStreamSynchronize(s));
     // stable LSD radix sort with ping-pong buffers (no n-sized CUB scratch)
     cub::DoubleBuffer<uint32_t> kb(rkey, skey);
     cub::DoubleBuffer<int32_t> vb(ridx, sidx);
-    b = L.cub_bytes;
-    int bits = 1;
-    while (bits < 32 && ((uint64_t)L.cells >> bits) != 0) ++bits;
-    // valid keys are < cells < 2^bits and invalid ones (0xffffffff) are all-ones in
-    // the low `bits` bits, so sorting those bits keeps the invalid runs last
-    GP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, b, kb, vb, (int)R, 0, bits, s));
+    size_t b = L.cub_bytes;
+    // stable sort by the block bits only: valid blocks are < k < 2^bb - 1 and the
+    // invalid key is all-ones there, so the invalid runs stay last
+    GP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, b, kb, vb, (int)R, 0, block_bits(f->k), s));
     skey = kb.Current();
     sidx = vb.Current();
     if (skey != (uint32_t*)(ws + L.off_skey_final)) {
@@ -587,8 +599,9 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     else GP_FOLD(3, 5, 1, 8);
   }
 #undef GP_FOLD
-  if (f->d == 2) fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
-  else fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out);
+  const int bbk = block_bits(f->k);
+  if (f->d == 2) fold_combine<2><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out, bbk);
+  else fold_combine<3><<<grid_for(f->k, 4), 128, 0, s>>>(*f, slot, L.nseg, out, bbk);
   return check_launch("movement_fold");
 }
 

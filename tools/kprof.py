@@ -32,6 +32,10 @@ for e in prof.events():
     r[0] += 1
     r[1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
 tot = sum(v[1] for v in rows.values())
+longest = sorted(((e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total,
+                   e.name[:60]) for e in prof.events() if e.device_type.name == "CUDA"),
+                 reverse=True)[:12]
+print("longest launches (ms):", [(round(t / 1e3, 2), n) for t, n in longest])
 print("API calls:", dict(sorted(N0.calls.items())))
 print(f"{'kernel':72s} {'calls':>6s} {'ms':>10s} {'%':>6s}")
 for k, v in sorted(rows.items(), key=lambda x: -x[1][1])[:25]:
