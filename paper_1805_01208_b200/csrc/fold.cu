@@ -49,7 +49,7 @@ struct FoldLayout {
 };
 
 constexpr int RT = 256;             // run extraction: threads per tile
-constexpr int RPER = 16;            // positions per thread
+constexpr int RPER = 16;            // entries per thread (4 chunks of 4)
 constexpr int RTILE = RT * RPER;    // positions per tile
 
 static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k) {
@@ -94,110 +94,127 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   return L;
 }
 
-// (segment, block) keys of a thread's RPER consecutive entries and the bit mask
-// of those that start a run (key differs from the previous entry's).  Key -1:
-// unassigned / inactive.  Entries are local positions i (list == NULL, one
-// segment computation per thread) or dense entries at positions list[i].
-__device__ __forceinline__ unsigned run_marks(const gp_fold_args& f, int64_t cnt, int64_t s0,
-                                              int64_t i0, int32_t (&key)[RPER]) {
-  int av[RPER];
-  if (i0 + RPER <= cnt) {
-    const int4* ap = reinterpret_cast<const int4*>(f.a + i0);
-#pragma unroll
-    for (int h = 0; h < RPER / 4; ++h) {
-      const int4 v = ap[h];
-      av[4 * h] = v.x; av[4 * h + 1] = v.y; av[4 * h + 2] = v.z; av[4 * h + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < RPER; ++e) av[e] = i0 + e < cnt ? f.a[i0 + e] : -1;
-  }
-  auto seg_at = [&](int64_t i) { return segment_of(f.pos0 + (f.list ? f.list[i] : i), f.n_global); };
-  int prev = -2;
-  if (i0 > 0) {
-    const int c = f.a[i0 - 1];
-    prev = c >= 0 ? (int)(((seg_at(i0 - 1) - s0) << block_bits(f.k)) | c) : -1;
-  }
-  int seg = 0;
-  int64_t next_b = 0;
-  if (!f.list) {
-    seg = segment_of(f.pos0 + i0, f.n_global);
-    next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * f.n_global >> 8) - f.pos0 : INT64_MAX;
-  }
-  unsigned m = 0;
-  const int bb = block_bits(f.k);
-#pragma unroll
-  for (int e = 0; e < RPER; ++e) {
-    const int64_t i = i0 + e;
-    if (i >= cnt) {
-      key[e] = -1;
-      continue;
-    }
-    int sg;
-    if (f.list) {
-      sg = av[e] >= 0 ? seg_at(i) : 0;
-    } else {
-      while (i >= next_b) {
-        ++seg;
-        next_b = seg + 1 < GP_SEGMENTS ? ((int64_t)(seg + 1) * f.n_global >> 8) - f.pos0
-                                       : INT64_MAX;
-      }
-      sg = seg;
-    }
-    const int kk = av[e] >= 0 ? (int)(((sg - s0) << bb) | av[e]) : -1;
-    key[e] = kk;
-    if (kk != prev) m |= 1u << e;
-    prev = kk;
-  }
-  return m;
-}
-
 typedef cub::ScanTileState<int> RunTiles;
 
 __global__ void run_tiles_init(RunTiles ts, int ntiles) { ts.InitializeStatus(ntiles); }
 
+// key of entry i (segment of its position, block); -1: unassigned / inactive
+__device__ __forceinline__ int32_t entry_key(const gp_fold_args& f, int64_t i, int c, int64_t s0,
+                                             int bb) {
+  if (c < 0) return -1;
+  const int sg = segment_of(f.pos0 + (f.list ? f.list[i] : i), f.n_global);
+  return (int32_t)(((sg - s0) << bb) | c);
+}
+
 // One pass over a: run r (in entry order) -> starts[r] = first entry, (key, r) for
-// the sort; the tile offsets come from a decoupled look-back over the tiles'
-// run counts.  Runs with key -1 (unassigned / inactive) sort last.
+// the sort.  Warp w of a tile owns 512 consecutive entries as four 128-entry chunks
+// (lane l: entries 4l..4l+3 of a chunk, one coalesced 16-byte load); run offsets
+// come from warp scans, a block scan over the warps and a decoupled look-back over
+// the tiles.  Runs with key -1 (unassigned / inactive) sort last.
 __global__ void __launch_bounds__(RT) run_single(gp_fold_args f, int64_t cnt, int64_t s0,
                                                  RunTiles ts, int64_t ntiles,
                                                  int32_t* __restrict__ starts,
                                                  uint32_t* __restrict__ rkey,
                                                  int32_t* __restrict__ ridx, int64_t* counters) {
-  typedef cub::BlockScan<int, RT> Scan;
   typedef cub::TilePrefixCallbackOp<int, ::cuda::std::plus<int>, RunTiles> Prefix;
-  __shared__ typename Scan::TempStorage tmp;
   __shared__ typename Prefix::TempStorage ptmp;
+  __shared__ int s_warp[RT / 32];
+  __shared__ int s_tile_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
-  const int64_t i0 = (int64_t)tile * RTILE + (int64_t)threadIdx.x * RPER;
-  int32_t key[RPER];
-  const unsigned m = i0 < cnt ? run_marks(f, cnt, s0, i0, key) : 0u;
-  int excl;
-  if (tile == 0) {
-    int agg;
-    Scan(tmp).ExclusiveSum(__popc(m), excl, agg);
-    if (threadIdx.x == 0) ts.SetInclusive(0, agg);
-  } else {
-    Prefix op(ts, ptmp, ::cuda::std::plus<int>(), tile);
-    Scan(tmp).ExclusiveSum(__popc(m), excl, op);
+  const int bb = block_bits(f.k);
+  const int64_t wbase = (int64_t)tile * RTILE + (int64_t)warp * (RTILE / (RT / 32));
+  // segment of the warp's first entry and the next boundary (dense entries)
+  int wseg = 0;
+  int64_t wnext = INT64_MAX;
+  if (!f.list && wbase < cnt) {
+    wseg = segment_of(f.pos0 + wbase, f.n_global);
+    wnext = wseg + 1 < GP_SEGMENTS ? ((int64_t)(wseg + 1) * f.n_global >> 8) - f.pos0 : INT64_MAX;
   }
-  int r = excl;
+  auto key_of = [&](int64_t i, int c) -> int32_t {
+    if (c < 0) return -1;
+    if (!f.list && i < wnext) return (int32_t)(((wseg - s0) << bb) | c);
+    return entry_key(f, i, c, s0, bb);
+  };
+  int32_t carry = -2;   // key of the entry before the current chunk (lane 0's predecessor)
+  if (lane == 0 && wbase > 0 && wbase <= cnt) carry = entry_key(f, wbase - 1, f.a[wbase - 1], s0, bb);
+  int32_t keys[4][4];
+  unsigned marks[4];
+  int excl[4];
+  int wsum = 0;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const int64_t e0 = wbase + 128 * h + 4 * lane;
+    int av[4];
+    if (e0 + 4 <= cnt) {
+      const int4 v = *reinterpret_cast<const int4*>(f.a + e0);
+      av[0] = v.x; av[1] = v.y; av[2] = v.z; av[3] = v.w;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) av[t] = e0 + t < cnt ? f.a[e0 + t] : -1;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) keys[h][t] = key_of(e0 + t, av[t]);
+    int32_t prev = __shfl_up_sync(FULL, keys[h][3], 1);
+    if (lane == 0) prev = carry;
+    carry = __shfl_sync(FULL, keys[h][3], 31);
+    unsigned m = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (e0 + t < cnt && keys[h][t] != (t == 0 ? prev : keys[h][t - 1])) m |= 1u << t;
+    }
+    marks[h] = m;
+    const int c = __popc(m);
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    excl[h] = wsum + incl - c;
+    wsum += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) s_warp[warp] = wsum;
+  __syncthreads();
+  int wpre = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < RT / 32; ++w) {
+    const int t = s_warp[w];
+    wpre += w < warp ? t : 0;
+    agg += t;
+  }
+  if (warp == 0) {
+    int pre = 0;
+    if (tile == 0) {
+      if (lane == 0) ts.SetInclusive(0, agg);
+    } else {
+      Prefix op(ts, ptmp, ::cuda::std::plus<int>(), tile);
+      pre = op(agg);
+    }
+    if (lane == 0) s_tile_prefix = pre;
+  }
+  __syncthreads();
+  const int base = s_tile_prefix + wpre;
   int valid = 0;
 #pragma unroll
-  for (int e = 0; e < RPER; ++e)
-    if (m & (1u << e)) {
-      starts[r] = (int32_t)(i0 + e);
-      rkey[r] = (uint32_t)key[e];
-      ridx[r] = r;
-      valid += key[e] >= 0;
-      ++r;
-    }
+  for (int h = 0; h < 4; ++h) {
+    int r = base + excl[h];
+    const int64_t e0 = wbase + 128 * h + 4 * lane;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (marks[h] & (1u << t)) {
+        starts[r] = (int32_t)(e0 + t);
+        rkey[r] = (uint32_t)keys[h][t];
+        ridx[r] = r;
+        valid += keys[h][t] >= 0;
+        ++r;
+      }
+  }
   for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(FULL, valid, o);
-  if ((threadIdx.x & 31) == 0 && valid)
-    atomicAdd((unsigned long long*)&counters[2], (unsigned long long)valid);
-  if (tile == ntiles - 1 && threadIdx.x == RT - 1) {
-    starts[r] = (int32_t)cnt;  // sentinel end (r = total runs)
-    counters[0] = r;
+  if (lane == 0 && valid) atomicAdd((unsigned long long*)&counters[2], (unsigned long long)valid);
+  if (tile == ntiles - 1 && threadIdx.x == 0) {
+    const int R = s_tile_prefix + agg;
+    starts[R] = (int32_t)cnt;  // sentinel end
+    counters[0] = R;
   }
 }
 
