@@ -17,9 +17,7 @@
 //              objective terms (kmeans.py:490-499) are computed in parallel
 //              by all lanes of the chunk;
 //   combine  : per block, fold the pair partials in segment order.
-#include <cub/agent/single_pass_scan_operators.cuh>
 #include <cub/block/block_scan.cuh>
-#include <cuda/std/functional>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -45,7 +43,7 @@ __host__ __device__ __forceinline__ int block_bits(int k) {
 struct FoldLayout {
   int64_t s0, nseg, cells, cap, pcap, ntiles;
   size_t off_flags, off_starts, off_rkey, off_skey, off_sidx, off_ridx, off_pbeg, off_slot,
-      off_out, off_counters, off_cub, cub_bytes, off_tiles, off_skey_final, total;
+      off_out, off_counters, off_cub, cub_bytes, off_tiles, off_mask, off_skey_final, total;
 };
 
 constexpr int RT = 256;             // run extraction: threads per tile
@@ -87,16 +85,11 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   L.off_out = o; o = al(o + L.pcap * (MAXCOL + 1) * sizeof(double));
   L.off_counters = o; o = al(o + 8 * sizeof(int64_t));
   L.off_cub = o; o = al(o + L.cub_bytes);
-  size_t tsb = 0;
-  cub::ScanTileState<int>::AllocationSize((int)L.ntiles, tsb);
-  L.off_tiles = o; o = al(o + tsb);
+  L.off_tiles = o; o = al(o + (L.ntiles + 1) * 4);
+  L.off_mask = o; o = al(o + L.ntiles * (RTILE / 8));
   L.total = o;
   return L;
 }
-
-typedef cub::ScanTileState<int> RunTiles;
-
-__global__ void run_tiles_init(RunTiles ts, int ntiles) { ts.InitializeStatus(ntiles); }
 
 // key of entry i (segment of its position, block); -1: unassigned / inactive
 __device__ __forceinline__ int32_t entry_key(const gp_fold_args& f, int64_t i, int c, int64_t s0,
@@ -106,25 +99,17 @@ __device__ __forceinline__ int32_t entry_key(const gp_fold_args& f, int64_t i, i
   return (int32_t)(((sg - s0) << bb) | c);
 }
 
-// One pass over a: run r (in entry order) -> starts[r] = first entry, (key, r) for
-// the sort.  Warp w of a tile owns 512 consecutive entries as four 128-entry chunks
-// (lane l: entries 4l..4l+3 of a chunk, one coalesced 16-byte load); run offsets
-// come from warp scans, a block scan over the warps and a decoupled look-back over
-// the tiles.  Runs with key -1 (unassigned / inactive) sort last.
-__global__ void __launch_bounds__(RT) run_single(gp_fold_args f, int64_t cnt, int64_t s0,
-                                                 RunTiles ts, int64_t ntiles,
-                                                 int32_t* __restrict__ starts,
-                                                 uint32_t* __restrict__ rkey,
-                                                 int32_t* __restrict__ ridx, int64_t* counters) {
-  typedef cub::TilePrefixCallbackOp<int, ::cuda::std::plus<int>, RunTiles> Prefix;
-  __shared__ typename Prefix::TempStorage ptmp;
+// Pass 1 (streams a once): bit i of mask = entry i starts a run (its key differs from
+// its predecessor's), tiles[t] = run starts in tile t (RTILE entries).  Warp w of a
+// tile owns 512 consecutive entries as four 128-entry chunks (lane l: entries
+// 4l..4l+3 of a chunk, one coalesced 16-byte load).
+__global__ void __launch_bounds__(RT) run_mark(gp_fold_args f, int64_t cnt, int64_t s0,
+                                               uint32_t* __restrict__ mask,
+                                               int32_t* __restrict__ tiles) {
   __shared__ int s_warp[RT / 32];
-  __shared__ int s_tile_prefix;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile = blockIdx.x;
   const int bb = block_bits(f.k);
-  const int64_t wbase = (int64_t)tile * RTILE + (int64_t)warp * (RTILE / (RT / 32));
-  // segment of the warp's first entry and the next boundary (dense entries)
+  const int64_t wbase = (int64_t)blockIdx.x * RTILE + (int64_t)warp * (RTILE / (RT / 32));
   int wseg = 0;
   int64_t wnext = INT64_MAX;
   if (!f.list && wbase < cnt) {
@@ -138,10 +123,7 @@ __global__ void __launch_bounds__(RT) run_single(gp_fold_args f, int64_t cnt, in
   };
   int32_t carry = -2;   // key of the entry before the current chunk (lane 0's predecessor)
   if (lane == 0 && wbase > 0 && wbase <= cnt) carry = entry_key(f, wbase - 1, f.a[wbase - 1], s0, bb);
-  int32_t keys[4][4];
-  unsigned marks[4];
-  int excl[4];
-  int wsum = 0;
+  int total = 0;
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     const int64_t e0 = wbase + 128 * h + 4 * lane;
@@ -153,66 +135,73 @@ __global__ void __launch_bounds__(RT) run_single(gp_fold_args f, int64_t cnt, in
 #pragma unroll
       for (int t = 0; t < 4; ++t) av[t] = e0 + t < cnt ? f.a[e0 + t] : -1;
     }
+    int32_t key[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) keys[h][t] = key_of(e0 + t, av[t]);
-    int32_t prev = __shfl_up_sync(FULL, keys[h][3], 1);
+    for (int t = 0; t < 4; ++t) key[t] = key_of(e0 + t, av[t]);
+    int32_t prev = __shfl_up_sync(FULL, key[3], 1);
     if (lane == 0) prev = carry;
-    carry = __shfl_sync(FULL, keys[h][3], 31);
-    unsigned m = 0;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (e0 + t < cnt && keys[h][t] != (t == 0 ? prev : keys[h][t - 1])) m |= 1u << t;
-    }
-    marks[h] = m;
-    const int c = __popc(m);
-    int incl = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    excl[h] = wsum + incl - c;
-    wsum += __shfl_sync(FULL, incl, 31);
-  }
-  if (lane == 0) s_warp[warp] = wsum;
-  __syncthreads();
-  int wpre = 0, agg = 0;
-#pragma unroll
-  for (int w = 0; w < RT / 32; ++w) {
-    const int t = s_warp[w];
-    wpre += w < warp ? t : 0;
-    agg += t;
-  }
-  if (warp == 0) {
-    int pre = 0;
-    if (tile == 0) {
-      if (lane == 0) ts.SetInclusive(0, agg);
-    } else {
-      Prefix op(ts, ptmp, ::cuda::std::plus<int>(), tile);
-      pre = op(agg);
-    }
-    if (lane == 0) s_tile_prefix = pre;
-  }
-  __syncthreads();
-  const int base = s_tile_prefix + wpre;
-  int valid = 0;
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    int r = base + excl[h];
-    const int64_t e0 = wbase + 128 * h + 4 * lane;
+    carry = __shfl_sync(FULL, key[3], 31);
+    unsigned b[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t)
-      if (marks[h] & (1u << t)) {
-        starts[r] = (int32_t)(e0 + t);
-        rkey[r] = (uint32_t)keys[h][t];
-        ridx[r] = r;
-        valid += keys[h][t] >= 0;
-        ++r;
+      b[t] = __ballot_sync(FULL, e0 + t < cnt && key[t] != (t == 0 ? prev : key[t - 1]));
+    total += __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]);
+    // entry 4l + t of the chunk is bit t of lane l's nibble: word w = lanes 8w..8w+7
+    if (lane < 4) {
+      unsigned word = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const unsigned byte = (b[t] >> (8 * lane)) & 0xffu;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) word |= ((byte >> j) & 1u) << (4 * j + t);
       }
+      if (wbase + 128 * h < cnt) mask[(wbase + 128 * h) / 32 + lane] = word;
+    }
+  }
+  if (lane == 0) s_warp[warp] = total;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < RT / 32; ++w) t += s_warp[w];
+    tiles[blockIdx.x] = t;
+  }
+}
+
+// Pass 2 (reads only the mask and the run-start entries): run r in entry order ->
+// starts[r], (key, r) for the sort; one thread per 32-entry mask word.
+constexpr int WT2 = RTILE / 32;   // mask words per tile (128)
+__global__ void __launch_bounds__(WT2) run_emit(gp_fold_args f, int64_t cnt, int64_t s0,
+                                                const uint32_t* __restrict__ mask,
+                                                const int32_t* __restrict__ tile_off,
+                                                int64_t ntiles, int32_t* __restrict__ starts,
+                                                uint32_t* __restrict__ rkey,
+                                                int32_t* __restrict__ ridx, int64_t* counters) {
+  typedef cub::BlockScan<int, WT2> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const int bb = block_bits(f.k);
+  const int64_t wi = (int64_t)blockIdx.x * WT2 + threadIdx.x;   // mask word
+  const int64_t e0 = wi * 32;
+  unsigned w = e0 < cnt ? mask[wi] : 0u;
+  int excl;
+  Scan(tmp).ExclusiveSum(__popc(w), excl);
+  int r = tile_off[blockIdx.x] + excl;
+  int valid = 0;
+  while (w) {
+    const int t = __ffs(w) - 1;
+    w &= w - 1;
+    const int64_t i = e0 + t;
+    const int32_t key = entry_key(f, i, f.a[i], s0, bb);
+    starts[r] = (int32_t)i;
+    rkey[r] = (uint32_t)key;
+    ridx[r] = r;
+    valid += key >= 0;
+    ++r;
   }
   for (int o = 16; o; o >>= 1) valid += __shfl_xor_sync(FULL, valid, o);
-  if (lane == 0 && valid) atomicAdd((unsigned long long*)&counters[2], (unsigned long long)valid);
-  if (tile == ntiles - 1 && threadIdx.x == 0) {
-    const int R = s_tile_prefix + agg;
+  if ((threadIdx.x & 31) == 0 && valid)
+    atomicAdd((unsigned long long*)&counters[2], (unsigned long long)valid);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int R = tile_off[ntiles];
     starts[R] = (int32_t)cnt;  // sentinel end
     counters[0] = R;
   }
@@ -553,12 +542,14 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
   GP_CUDA(cudaMemsetAsync(slot, 0xff, L.cells * sizeof(int32_t), s));
   if (cnt > 0) {
     const int64_t nt = (cnt + RTILE - 1) / RTILE;
-    RunTiles ts;
-    size_t tsb = 0;
-    RunTiles::AllocationSize((int)nt, tsb);
-    GP_CUDA(ts.Init((int)nt, ws + L.off_tiles, tsb));
-    run_tiles_init<<<grid_for(nt, 256), 256, 0, s>>>(ts, (int)nt);
-    run_single<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, ts, nt, starts, rkey, ridx, counters);
+    int32_t* tiles = (int32_t*)(ws + L.off_tiles);
+    uint32_t* mask = (uint32_t*)(ws + L.off_mask);
+    run_mark<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, mask, tiles);
+    GP_CUDA(cudaMemsetAsync(tiles + nt, 0, sizeof(int32_t), s));
+    size_t sb = L.cub_bytes;
+    GP_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, sb, tiles, tiles, (int)nt + 1, s));
+    run_emit<<<(unsigned)nt, WT2, 0, s>>>(*f, cnt, L.s0, mask, tiles, nt, starts, rkey, ridx,
+                                         counters);
     int64_t R = 0;
     GP_CUDA(cudaMemcpyAsync(&R, counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     GP_CUDA(cudaStreamSynchronize(s));
