@@ -8,6 +8,8 @@
 #include <cstdarg>
 #include <cstdio>
 
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 
 namespace gp {
@@ -204,82 +206,48 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, int64_t ldx, in
 }
 
 // ------------------------------------------------------- K5 compaction
-constexpr int CT_THREADS = 256;
-constexpr int CT_ROUNDS = 16;
-constexpr int CT_TILE = CT_THREADS * CT_ROUNDS;
+// Ordered compaction of {i : rank[i] < size} in two passes over warp chunks of
+// CW = 512 consecutive entries (no block-wide barriers): per-chunk counts, a device
+// scan of the counts, then every warp writes its chunk's indices by ballot.
+constexpr int CW = 512;
 
 __global__ void compact_count(const int32_t* __restrict__ rank, int64_t n, int64_t size,
-                              int64_t* counts) {
-  int64_t base = (int64_t)blockIdx.x * CT_TILE;
+                              int64_t* __restrict__ counts, int64_t nch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (ch >= nch) return;
   int c = 0;
-  for (int r = 0; r < CT_ROUNDS; ++r) {
-    int64_t i = base + r * CT_THREADS + threadIdx.x;
+#pragma unroll
+  for (int r = 0; r < CW / 32; ++r) {
+    const int64_t i = ch * CW + r * 32 + lane;
     c += (i < n && rank[i] < size);
   }
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-  __shared__ int ws[CT_THREADS / 32];
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < CT_THREADS / 32; ++w) t += ws[w];
-    counts[blockIdx.x] = t;
-  }
-}
-
-__global__ void exclusive_scan_serial(int64_t* counts, int64_t m, int64_t* total) {
-  // single block: chunked scan
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < m; base += blockDim.x) {
-    int64_t i = base + threadIdx.x;
-    int64_t v = i < m ? counts[i] : 0;
-    // block inclusive scan (Hillis-Steele in smem)
-    __shared__ int64_t buf[1024];
-    buf[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-      int64_t t = threadIdx.x >= (unsigned)o ? buf[threadIdx.x - o] : 0;
-      __syncthreads();
-      buf[threadIdx.x] += t;
-      __syncthreads();
-    }
-    if (i < m) counts[i] = carry + buf[threadIdx.x] - v;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry += buf[threadIdx.x];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total = carry;
+  if (lane == 0) counts[ch] = c;
 }
 
 __global__ void compact_write(const int32_t* __restrict__ rank, int64_t n, int64_t size,
-                              const int64_t* __restrict__ offsets, int32_t* __restrict__ idx) {
-  __shared__ int wsum[CT_THREADS / 32];
-  __shared__ int64_t run;
-  int64_t base = (int64_t)blockIdx.x * CT_TILE;
-  if (threadIdx.x == 0) run = offsets[blockIdx.x];
-  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();
-  for (int r = 0; r < CT_ROUNDS; ++r) {
-    int64_t i = base + r * CT_THREADS + threadIdx.x;
-    bool f = i < n && rank[i] < size;
-    unsigned b = __ballot_sync(FULL, f);
-    if (lane == 0) wsum[warp] = __popc(b);
-    __syncthreads();
-    int before = 0, tot = 0;
-    for (int w = 0; w < CT_THREADS / 32; ++w) {
-      before += (w < warp) ? wsum[w] : 0;
-      tot += wsum[w];
-    }
-    if (f) idx[run + before + __popc(b & ((1u << lane) - 1))] = (int32_t)i;
-    __syncthreads();
-    if (threadIdx.x == 0) run += tot;
-    __syncthreads();
+                              const int64_t* __restrict__ offsets, int64_t nch,
+                              int32_t* __restrict__ idx, int64_t* __restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (ch == 0 && lane == 0) *total = offsets[nch];
+  if (ch >= nch) return;
+  int64_t run = offsets[ch];
+  bool f[CW / 32];
+#pragma unroll
+  for (int r = 0; r < CW / 32; ++r) {
+    const int64_t i = ch * CW + r * 32 + lane;
+    f[r] = i < n && rank[i] < size;
+  }
+#pragma unroll
+  for (int r = 0; r < CW / 32; ++r) {
+    const unsigned b = __ballot_sync(FULL, f[r]);
+    if (f[r]) idx[run + __popc(b & ((1u << lane) - 1))] = (int32_t)(ch * CW + r * 32 + lane);
+    run += __popc(b);
   }
 }
 
-// --------------------------------------------------------- scatter / gather
 __global__ void scatter_gid_kernel(const int32_t* __restrict__ a, const uint32_t* __restrict__ g,
                                    int64_t n, int64_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -441,26 +409,38 @@ int gp_gather_rows(const double* X, int64_t ldx, int d, const int64_t* positions
   return check_launch("gather_rows");
 }
 
+static size_t compact_scan_bytes(int64_t nch) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)nch + 1);
+  return b;
+}
+
 int gp_compact_workspace_bytes(int64_t n, size_t* bytes) {
-  int64_t tiles = (n + CT_TILE - 1) / CT_TILE;
-  *bytes = (size_t)(tiles + 1) * sizeof(int64_t);
+  const int64_t nch = (n + CW - 1) / CW;
+  *bytes = ((size_t)(nch + 1) * sizeof(int64_t) + 255) / 256 * 256 + compact_scan_bytes(nch);
   return GP_OK;
 }
 
 int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx, int64_t* count,
                       void* workspace, size_t workspace_bytes, void* stream) {
-  int64_t tiles = (n + CT_TILE - 1) / CT_TILE;
-  GP_REQUIRE(workspace_bytes >= (size_t)(tiles + 1) * sizeof(int64_t),
-             "gp_compact_active: workspace too small");
+  const int64_t nch = (n + CW - 1) / CW;
+  size_t need = 0;
+  gp_compact_workspace_bytes(n, &need);
+  GP_REQUIRE(workspace_bytes >= need, "gp_compact_active: workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
   if (n == 0) {
     GP_CUDA(cudaMemsetAsync(count, 0, sizeof(int64_t), s));
     return GP_OK;
   }
   int64_t* counts = (int64_t*)workspace;
-  compact_count<<<(unsigned)tiles, CT_THREADS, 0, s>>>(rank, n, size, counts);
-  exclusive_scan_serial<<<1, 1024, 0, s>>>(counts, tiles, count);
-  compact_write<<<(unsigned)tiles, CT_THREADS, 0, s>>>(rank, n, size, counts, idx);
+  void* tmp = (char*)workspace + ((size_t)(nch + 1) * sizeof(int64_t) + 255) / 256 * 256;
+  const unsigned g = (unsigned)((nch * 32 + 255) / 256);
+  compact_count<<<g, 256, 0, s>>>(rank, n, size, counts, nch);
+  GP_CUDA(cudaMemsetAsync(counts + nch, 0, sizeof(int64_t), s));
+  size_t tb = compact_scan_bytes(nch);
+  GP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, counts, (int)nch + 1, s));
+  compact_write<<<g, 256, 0, s>>>(rank, n, size, counts, nch, idx, count);
   return check_launch("compact_active");
 }
 

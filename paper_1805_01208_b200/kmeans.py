@@ -675,9 +675,8 @@ class DevicePartitioner:
             info = BalanceInfo(rounds, final_imb, block_w, skips, decisions, evals, history)
             self._leave_dense()
             if phase == "full" and info.imbalance <= st.epsilon:
-                if fallback is None:
-                    self.A_fb = torch.empty_like(self.A)
-                self.A_fb.copy_(self.A)
+                # the assignment at this point is the exact argmin under (centers, infl);
+                # it is recomputed from them only if the fallback is taken (no n-sized copy)
                 fallback = (ClusterState(centers.copy(), infl.copy(), block_w.copy(),
                                          last_move.copy()), info.imbalance)
             # ---------------- movement (kmeans.py:585-626)
@@ -731,8 +730,8 @@ class DevicePartitioner:
         final_imb = info.imbalance
         A = self.A
         if final_imb > st.epsilon and fallback is not None:
-            A = self.A_fb
             final_state, final_imb = fallback
+            A = self._recompute(final_state)
         stats.balance_failed = final_imb > st.epsilon
         stats.final_state = final_state
         if st.audit_bounds:
@@ -744,6 +743,18 @@ class DevicePartitioner:
         self.release()
         return out, stats
 
+    def _recompute(self, state: ClusterState):
+        """The fallback assignment (kmeans.py:583-584, 627-630): one assign round from
+        cold bounds under the fallback centers and influences reproduces it exactly."""
+        self.centers_d.copy_(torch.from_numpy(np.ascontiguousarray(state.centers)))
+        self._build_grid(state.centers)
+        self._set_influence(state.influence, reset=True)
+        self.UBLB[:, 0] = math.inf
+        self.UBLB[:, 1] = 0.0
+        self.lists_fresh = False
+        self._assign()
+        return self.A
+
     def _deliver(self, A):
         """int64 assignment by original id (kmeans.py:637-641)."""
         out = torch.empty(self.n, dtype=torch.int64, device=self.device)
@@ -753,7 +764,7 @@ class DevicePartitioner:
 
     def release(self):
         """Drop every n-sized device buffer (the caller keeps only the result)."""
-        for name in ("X", "W", "A", "A_fb", "UBLB", "A_d", "UBLB_d", "X_d", "W_d", "gids", "rank_sfc", "active_idx",
+        for name in ("X", "W", "A", "UBLB", "A_d", "UBLB_d", "X_d", "W_d", "gids", "rank_sfc", "active_idx",
                      "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier", "grid_start",
                      "grid_items", "ubox", "rstate", "rpar"):
             if hasattr(self, name):
@@ -936,6 +947,18 @@ class DistributedPartitioner(DevicePartitioner):
         N.call("gp_fold_combine", keys.data_ptr(), vals.data_ptr(), keys.shape[0], k, d,
                weights_only, fo, fo + 8 * k * d, fo + 8 * k * (d + 1), fo + 8 * k * (d + 2),
                self.combine_ws.data_ptr(), self.combine_ws.numel(), self.sh)
+
+    def _recompute(self, state: ClusterState):
+        """The fallback assignment (kmeans.py:583-584, 627-630): one assign round from
+        cold bounds under the fallback centers and influences reproduces it exactly."""
+        self.centers_d.copy_(torch.from_numpy(np.ascontiguousarray(state.centers)))
+        self._build_grid(state.centers)
+        self._set_influence(state.influence, reset=True)
+        self.UBLB[:, 0] = math.inf
+        self.UBLB[:, 1] = 0.0
+        self.lists_fresh = False
+        self._assign()
+        return self.A
 
     def _deliver(self, A):
         """Labels of this rank's own input rows, routed back from the SFC shards."""

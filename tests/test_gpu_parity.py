@@ -219,6 +219,28 @@ def test_bound_audit_region_maps():
     assert total >= 1_000_000 and viol == 0 and badskip == 0
 
 
+@pytest.mark.parametrize("seed,k,eps,mbi,mi", [(2, 8, 0.02, 3, 4), (2, 16, 0.02, 2, 8),
+                                                (3, 8, 0.01, 2, 8), (4, 8, 0.02, 2, 4)])
+def test_fallback_state_bit_exact(seed, k, eps, mbi, mi):
+    """The last full iteration misses epsilon after an earlier one met it: the result is
+    the fallback snapshot (kmeans.py:583-584, 627-630), recomputed on the device."""
+    O = _oracle()
+    rng = np.random.default_rng(seed)
+    pts = rng.random((3000, 2)) if seed % 2 == 0 else rng.normal(size=(3000, 2))
+    ref = O.run(pts, None, O.Knobs(k=k, epsilon=eps, max_balance_iter=mbi, max_iter=mi,
+                                   seed=seed, init_sample=100))
+    full = [r for r in ref.records if r["phase"] == "full"]
+    assert full[-1]["imbalance"] > eps and any(r["imbalance"] <= eps for r in full[:-1])
+    part, stats = balanced_kmeans_points(
+        pts, None, KMeansSettings(k=k, epsilon=eps, max_balance_iter=mbi, max_iter=mi, seed=seed),
+        return_stats=True)
+    assert np.array_equal(part.assignment, ref.assignment)
+    assert part.balance_failed == ref.balance_failed
+    assert np.array_equal(stats.final_state.centers, ref.centers)
+    assert np.array_equal(stats.final_state.influence, ref.influence)
+    assert np.array_equal(stats.final_state.block_weights, ref.block_weights)
+
+
 def test_pruning_rate():
     """ACCEPT-06 analogue: skip fraction >= 0.5 over the last three iterations."""
     rng = np.random.default_rng(0)
