@@ -297,45 +297,74 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
         lb[e] = v.y;
       }
     }
-    // skip test + run-length block weights of the kept points (at most two runs per
-    // lane are held; a third, which needs three blocks among 8 entries, goes to
-    // global memory directly)
+    // skip test + block weights of the kept points.  Fast path (most lanes): all 8
+    // entries valid and in one block, so one parameter load and a branch-free skip
+    // mask.  General path: run-length weights (at most two runs per lane are held; a
+    // third, which needs three blocks among 8 entries, goes to global memory directly).
     unsigned need = 0;
     int run_a = -1, run2_a = -1;
     RunW run_w = 0, run2_w = 0;
-    int ea = -1;          // block whose bound parameters E holds (runs share them)
-    float4 E = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool same = staged && a[0] >= 0;
 #pragma unroll
-    for (int e = 0; e < FPER; ++e) {
-      const bool valid = staged || q[e] >= 0;
-      const int ae = a[e];
-      if (ae >= 0 && ae != ea) {
-        E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
-        ea = ae;
+    for (int e = 1; e < FPER; ++e) same = same && a[e] == a[0];
+    if (same) {
+      const float4 E = reinterpret_cast<const float4*>(p.ub_eval)[a[0]];
+      unsigned keep = 0;
+#pragma unroll
+      for (int e = 0; e < FPER; ++e) {
+        // lb_evalf without its k == 1 test: A > 0 maps lb~ = inf to inf as well
+        const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
+        keep |= (unsigned)(ub_evalf(E, ub[e]) < lbv) << e;
       }
-      // lb_evalf without its k == 1 test: A > 0 maps lb~ = inf to inf as well
-      const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
-      const bool skip = valid && ae >= 0 && ub_evalf(E, ub[e]) < lbv;
-      need |= (unsigned)(valid && !skip) << e;
-      if (skip) {
-        const RunW v = (RunW)weight_units<WM>(p.w, q[e], wshift);
-        if (ae == run_a) {
-          run_w += v;
+      need = keep ^ ((1u << FPER) - 1);
+      if (keep) {
+        run_a = a[0];
+        if (WM == GP_W_UNIT) {
+          run_w = (RunW)__popc(keep);
         } else {
-          if (run_a >= 0) {
-            if (run2_a >= 0)
-              atomicAdd((unsigned long long*)&p.block_w[run2_a], (unsigned long long)run2_w);
-            run2_a = run_a;
-            run2_w = run_w;
+#pragma unroll
+          for (int e = 0; e < FPER; ++e)
+            if (keep & (1u << e)) run_w += (RunW)weight_units<WM>(p.w, q[e], wshift);
+        }
+      }
+    } else {
+      int ea = -1;          // block whose bound parameters E holds (runs share them)
+      float4 E = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < FPER; ++e) {
+        const bool valid = staged || q[e] >= 0;
+        const int ae = a[e];
+        if (ae >= 0 && ae != ea) {
+          E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
+          ea = ae;
+        }
+        const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
+        const bool skip = valid && ae >= 0 && ub_evalf(E, ub[e]) < lbv;
+        need |= (unsigned)(valid && !skip) << e;
+        if (skip) {
+          const RunW v = (RunW)weight_units<WM>(p.w, q[e], wshift);
+          if (ae == run_a) {
+            run_w += v;
+          } else {
+            if (run_a >= 0) {
+              if (run2_a >= 0)
+                atomicAdd((unsigned long long*)&p.block_w[run2_a], (unsigned long long)run2_w);
+              run2_a = run_a;
+              run2_w = run_w;
+            }
+            run_a = ae;
+            run_w = v;
           }
-          run_a = ae;
-          run_w = v;
         }
       }
     }
     nskip += nvalid - __popc(need);
     tab_add(tab, p.block_w, lane, run2_a >= 0, run2_a, run2_w);
     tab_add(tab, p.block_w, lane, run_a >= 0, run_a, run_w);
+    if (!__any_sync(FULL, need)) {   // nothing to rescan in this region (the common case)
+      if (lane == 0) runs[reg] = 0;
+      continue;
+    }
     // compaction of the points to scan into the region's own slots, in entry order
     // (entry 64h + 2l + b: ranks from two ballots per h)
     int32_t* dst = scan + (int64_t)reg * WREG;
