@@ -324,6 +324,31 @@ int gp_scatter_by_gid(const int32_t* a, const uint32_t* gids, int64_t n, int64_t
 int gp_gather_ranks(const int32_t* rank_by_gid, const uint32_t* gids, int64_t n, int32_t* out,
                     void* stream);
 
+/* ---- callers of the path ---------------------------------- */
+
+/* SFC baseline cut (baselines.py:62-89, replaces lines 84-89 after the key sort
+ * of lines 82-83): for curve position i (gids = the stable key sort's values)
+ *   before = cumsum(w)[i] - w[i], total = w.sum(),
+ *   labels[gids[i]] = min((int64)(before * k / total), k - 1).
+ * w is by original id (NULL = unit weights, then scale must be 1).
+ * scale > 0: every weight times scale is an exact integer and the total of those
+ *   integers is below 2^53 (gp_weight_probe), so the prefix sums are exact.
+ * scale == 0: the reference's summation orders are restated literally (numpy's
+ *   pairwise w.sum() and a sequential cumsum).
+ * workspace: gp_sfc_cut_workspace_bytes(n). */
+int gp_sfc_cut_workspace_bytes(int64_t n, size_t* bytes);
+int gp_sfc_cut(const uint32_t* gids, const double* w, int64_t n, int k, double scale,
+               int64_t* labels, void* workspace, size_t workspace_bytes, void* stream);
+
+/* GeographerPartitioner.predict (estimators.py:107-114):
+ *   labels[i] = argmin_c norm(X[i] - centers[c]) / influence[c]
+ * with linalg.norm's (dx^2 + dy^2) + dz^2 order and numpy argmin semantics
+ * (first minimum; a NaN wins).  X is AoS (n, d).  safe_influence != 0 asserts
+ * every influence is finite and in [1e-150, 1e150] (enables the fp64 ranking
+ * pass; otherwise every point is evaluated with the exact arithmetic). */
+int gp_predict(const double* X, int64_t n, int d, const double* centers, const double* influence,
+               int k, int safe_influence, int64_t* labels, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -428,3 +428,55 @@ def runner_up_gap(points, centers, infl):
         return np.full(points.shape[0], np.inf)
     part = np.partition(mat, 1, axis=1)
     return (part[:, 1] - part[:, 0]) / np.maximum(part[:, 1], 1e-300)
+
+
+# --------------------------------------------------------------------------
+# Callers of the path: SFC baseline cut and estimator predict
+# --------------------------------------------------------------------------
+
+def sfc_labels(coords, weights, k: int, depth: int | None = None) -> np.ndarray:
+    """The SFC baseline (baselines.py:62-89): prefix weight strictly before each
+    vertex in (key, id) order, block floor(before*k/total) clipped to k-1."""
+    coords = np.asarray(coords, dtype=np.float64)
+    w_all = np.asarray(weights, dtype=np.float64)
+    n, d = coords.shape
+    if not 1 <= k <= n:
+        raise OracleError(f"k={k} out of range 1..{n}")
+    depth = DEFAULT_DEPTH[d] if depth is None else depth
+    keys = hilbert_keys(coords, coords.min(axis=0), coords.max(axis=0), depth)
+    order = sfc_order(keys)
+    w = w_all[order]
+    before = np.cumsum(w) - w                      # sequential fold, then one subtraction
+    total = float(w.sum())                         # numpy pairwise sum
+    block = np.minimum((before * k / total).astype(np.int64), k - 1)
+    out = np.empty(n, dtype=np.int64)
+    out[order] = block
+    return out
+
+
+def predict_labels(X, centers, infl) -> np.ndarray:
+    """GeographerPartitioner.predict (estimators.py:107-114), one center at a
+    time: norm = sqrt((dx^2 + dy^2) + dz^2) (linalg.norm's reduction order),
+    divided by the influence; argmin keeps the first minimum and a NaN wins."""
+    X = np.asarray(X, dtype=np.float64)
+    C = np.asarray(centers, dtype=np.float64)
+    f = np.asarray(infl, dtype=np.float64)
+    best = np.full(X.shape[0], np.inf)
+    arg = np.zeros(X.shape[0], dtype=np.int64)
+    seen_nan = np.zeros(X.shape[0], dtype=bool)
+    with np.errstate(all="ignore"):
+        for c in range(C.shape[0]):
+            diff = X - C[c]
+            sq = diff * diff
+            s = sq[:, 0]
+            for j in range(1, X.shape[1]):
+                s = s + sq[:, j]
+            dist = np.sqrt(s) / f[c]
+            nan = np.isnan(dist) & ~seen_nan
+            win = ((dist < best) & ~seen_nan) | nan
+            if c == 0:
+                win = np.ones_like(win)
+            best = np.where(win, dist, best)
+            arg = np.where(win, c, arg)
+            seen_nan |= nan
+    return arg

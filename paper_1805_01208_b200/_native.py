@@ -89,6 +89,9 @@ _SIGS = {
                                   vp]),
     "gp_scatter_state": (C.c_int, [vp, i64, vp, vp, vp, vp, vp]),
     "gp_gather_ranks": (C.c_int, [vp, vp, i64, vp, vp]),
+    "gp_sfc_cut_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_sfc_cut": (C.c_int, [vp, vp, i64, C.c_int, f64, vp, vp, sz, vp]),
+    "gp_predict": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -128,6 +131,7 @@ KERNELS_PER_CALL = {
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
     "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 1, "gp_region_maps": 1, "gp_lb_remap": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
+    "gp_sfc_cut": 3, "gp_predict": 1,
 }
 _launches = [0]
 calls: dict[str, int] = {}   # API calls by name (tools/kprof.py)

@@ -124,3 +124,52 @@ def numerics_fingerprint():
     return dict(pow_exp=h.hexdigest()[:16],
                 einsum3=hashlib.sha256(e3.tobytes()).hexdigest()[:16],
                 numpy=np.__version__)
+
+
+# ---------------------------------------------------------------- callers (§8f)
+def sfc_cut_inputs():
+    """SFC-baseline cases: name -> (coords, weights, k, depth)."""
+    rng = np.random.default_rng(202)
+    out = {}
+    out["u2_unit_k6"] = (rng.random((120, 2)), np.ones(120), 6, None)
+    out["u2_int_k7"] = (rng.random((3001, 2)), rng.integers(1, 61, 3001).astype(float), 7, None)
+    out["u3_f32w_k33"] = (rng.random((4099, 3)),
+                          rng.uniform(1, 4, 4099).astype(np.float32).astype(np.float64), 33, None)
+    # inexact weights: the pairwise total and the sequential cumsum decide the bits
+    out["u2_f64w_k50"] = (rng.random((20000, 2)), rng.random(20000) * 3 + 1e-3, 50, None)
+    out["u3_f64w_k5"] = (rng.random((777, 3)), rng.exponential(1.0, 777), 5, None)
+    out["line_heavy_k2"] = (np.stack([np.linspace(0.01, 0.99, 4), np.full(4, 0.5)], axis=1),
+                            np.array([3.0, 1.0, 1.0, 1.0]), 2, None)
+    out["keqn_k7"] = (rng.random((7, 2)), np.ones(7), 7, None)
+    out["k1"] = (rng.random((50, 2)), rng.random(50), 1, None)
+    out["depth10_k4"] = (rng.random((400, 2)), np.ones(400), 4, 10)
+    grid = np.stack(np.meshgrid(np.arange(9.0), np.arange(9.0), np.arange(9.0),
+                                indexing="ij"), axis=-1).reshape(-1, 3)
+    out["grid3_dups_k3"] = (np.concatenate([grid, grid[:100]]), np.ones(829), 3, None)
+    return out
+
+
+def predict_inputs():
+    """predict cases: name -> (X, centers, influence)."""
+    rng = np.random.default_rng(303)
+    out = {}
+    for d, k, n in ((2, 5, 400), (3, 17, 2000), (2, 64, 5000), (3, 300, 3000), (2, 1, 10)):
+        X = rng.random((n, d))
+        C = rng.random((k, d))
+        f = rng.uniform(0.7, 1.4, k)
+        out[f"d{d}_k{k}"] = (X, C, f)
+    # duplicated centers with equal influence (exact ties -> lowest index),
+    # points on centers, points outside the box
+    C = rng.random((12, 2))
+    C[7] = C[3]
+    C[11] = C[3]
+    f = np.ones(12)
+    X = np.concatenate([rng.random((500, 2)), C, rng.normal(0.5, 3.0, (200, 2))])
+    out["ties_d2"] = (X, C, f)
+    C = rng.random((9, 3))
+    C[8] = C[2]
+    f = rng.uniform(0.9, 1.1, 9)
+    f[8] = f[2]
+    X = np.concatenate([rng.random((700, 3)), C])
+    out["ties_d3"] = (X, C, f)
+    return out
