@@ -71,6 +71,18 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(cfg):
+    """DRAM bytes of one captured assign round (ncu --set full, committed under
+    profiles/) next to that round's algorithmic bytes, or None."""
+    path = os.path.join(ROOT, "profiles", "round1", f"ncu_traffic_{cfg}.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t
+    except Exception:
+        return None
+
+
 def workload(cfg):
     from paper_1805_01208_b200.workloads import CONFIGS, GENERATORS
 
@@ -149,15 +161,63 @@ def cpu_sample(cfg, c=None, pts=None, w=None, budget_s=25.0):
                 seconds=dt)
 
 
+def _cpu_worker(cfg, budget_s, barrier, queue):
+    barrier.wait()
+    r = cpu_sample(cfg, budget_s=budget_s)
+    queue.put((r["value"] * 1e9 * r["seconds"], r["seconds"], r["sample"]))
+
+
+def reference_workers():
+    """Host threads the reference arm may use: every core this process may run on,
+    bounded by memory (one oracle sample peaks at ~0.3 GB RSS; 1 GB is budgeted)."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    try:
+        import psutil
+
+        mem = int(psutil.virtual_memory().available // (1 << 30)) // 2
+    except Exception:
+        mem = 8
+    return max(1, min(cores, mem, 256))
+
+
+def cpu_sample_parallel(cfg, workers, budget_s):
+    """The reference's numpy path is single-threaded (one simulated rank after the
+    other), so the most the host can do is run one independent sample per core:
+    W processes start together, value = all their point-assignments / the slowest."""
+    import multiprocessing as mp
+
+    for v in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ[v] = "1"
+    ctx = mp.get_context("spawn")
+    barrier, queue = ctx.Barrier(workers), ctx.Queue()
+    procs = [ctx.Process(target=_cpu_worker, args=(cfg, budget_s, barrier, queue))
+             for _ in range(workers)]
+    for p in procs:
+        p.start()
+    res = [queue.get() for _ in procs]
+    for p in procs:
+        p.join()
+    dec = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return dict(value=dec / wall / 1e9, seconds=wall, cores=workers,
+                sample=f"{workers} concurrent single-threaded samples, each: {res[0][2]}")
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    c, pts, w, _ = cpu_inputs(args.config)
+    from paper_1805_01208_b200.workloads import CONFIGS
+
+    c = CONFIGS[args.config]     # the arm's workload; each step times a bounded sample of it
+    workers = reference_workers()
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        s = cpu_sample(args.config, budget_s=10.0)
+        s = cpu_sample_parallel(args.config, workers, budget_s=10.0)
         if i >= args.warmup:
             vals.append(s["value"])
             last = s
@@ -169,7 +229,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SURVEY §8d recipe)",
         "config": {"workload": f"{args.config}: {DESCR[args.config]}", "n": int(c["n"]),
                    "d": int(c["d"]), "k": c["k"], "epsilon": c["epsilon"]},
-        "cpu_baseline": {"value": v, "unit": "Gpt/s", "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "Gpt/s", "cores": last["cores"], "kind": "port",
                          "sample": last["sample"]},
         "e2e": {"value": v, "unit": "Gpt/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -353,6 +413,7 @@ def run_b200(args):
         cpu.pop("seconds", None)
 
     if rank == 0:
+        tr = ncu_traffic(args.config)
         line = {
             "metric": "point-assignments/s", "value": value, "unit": "Gpt/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -368,7 +429,11 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "kernel": "gp_assign_round",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                         "traffic": None, "launches": launches_assign,
+                         "traffic": (tr["dram_bytes_per_round"][0] if tr else None),
+                         "traffic_alg_bytes": (tr["alg_bytes_per_round"][0] if tr else None),
+                         "traffic_source": (f"one full-phase round (round {tr['rounds'][0]}) of "
+                                            f"{args.config}: {tr['source']}" if tr else None),
+                         "launches": launches_assign,
                          "avg_launch_us": kern_ms * 1e3 / max(launches_assign, 1),
                          "alg_bytes_per_launch": alg_bytes / max(launches_assign, 1),
                          "fp64_flops_per_launch": flops / max(launches_assign, 1),
