@@ -185,19 +185,7 @@ typedef struct gp_assign_args {
    * lb_rpar[li >> lb_rshift] instead of lb_par; NULL: the global lb_par */
   const float* lb_rpar;
   int32_t lb_rshift;
-  /* region skip summaries (dense rounds, list == NULL): for every full 256-entry
-   * region r, rsum[4r..4r+3] = {block of all its entries or -1, max ub~ and min
-   * lb~ over its entries (order-preserving int keys of the floats), unused}.  A
-   * region whose summary proves ub < lb for every entry is skipped without
-   * reading its entries (its weight goes to its block whole).  The filter
-   * rebuilds the summary of every region it reads; the scan merges the fresh
-   * bounds of rescanned entries.  rsum_reset != 0: the summaries are stale
-   * (bounds renormalised, new active set): nothing is skipped, all rebuilt, and
-   * for weighted modes the region weights rweight[r] (int64 units) recomputed.
-   * NULL rsum: no summaries. */
-  int32_t rsum_reset;
-  int32_t* rsum;
-  long long* rweight;
+  int32_t pad2;
 } gp_assign_args;
 int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);
