@@ -124,17 +124,24 @@ __global__ void __launch_bounds__(RT) run_mark(gp_fold_args f, int64_t cnt, int6
   int32_t carry = -2;   // key of the entry before the current chunk (lane 0's predecessor)
   if (lane == 0 && wbase > 0 && wbase <= cnt) carry = entry_key(f, wbase - 1, f.a[wbase - 1], s0, bb);
   int total = 0;
+  // all four chunks' loads first: 64 bytes per lane in flight
+  int4 va[4];
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     const int64_t e0 = wbase + 128 * h + 4 * lane;
-    int av[4];
     if (e0 + 4 <= cnt) {
-      const int4 v = *reinterpret_cast<const int4*>(f.a + e0);
-      av[0] = v.x; av[1] = v.y; av[2] = v.z; av[3] = v.w;
+      va[h] = __ldcs(reinterpret_cast<const int4*>(f.a + e0));
     } else {
-#pragma unroll
-      for (int t = 0; t < 4; ++t) av[t] = e0 + t < cnt ? f.a[e0 + t] : -1;
+      va[h].x = e0 < cnt ? f.a[e0] : -1;
+      va[h].y = e0 + 1 < cnt ? f.a[e0 + 1] : -1;
+      va[h].z = e0 + 2 < cnt ? f.a[e0 + 2] : -1;
+      va[h].w = e0 + 3 < cnt ? f.a[e0 + 3] : -1;
     }
+  }
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const int64_t e0 = wbase + 128 * h + 4 * lane;
+    const int av[4] = {va[h].x, va[h].y, va[h].z, va[h].w};
     int32_t key[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) key[t] = key_of(e0 + t, av[t]);
