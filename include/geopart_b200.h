@@ -180,7 +180,10 @@ typedef struct gp_assign_args {
    * points are computed per round */
   const double* unit_boxes;
   int32_t unit_shift;
-  int32_t flags;          /* bit 0: accumulate scan statistics (gp_scan_stats) */
+  int32_t flags;          /* bit 0: accumulate scan statistics (gp_scan_stats);
+                             bit 1: sparse round: one warp per rescanned point walks
+                             the center grid (needs grid_n > 0) instead of the
+                             per-unit candidate scan */
   /* region-local lower-bound maps (gp_region_maps): entry li uses the float4
    * lb_rpar[li >> lb_rshift] instead of lb_par; NULL: the global lb_par */
   const float* lb_rpar;

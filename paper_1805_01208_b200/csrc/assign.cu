@@ -551,6 +551,183 @@ __device__ void grid_point(const gp_assign_args& p, const double* x, int& bi, fl
   secondf = __double2float_rd(second);
 }
 
+// ------------------------------------------------------------ walk kernel
+// Sparse warm-up rounds (flags bit 1: few active points per center): one warp per
+// rescanned point walks the center grid ring by ring around it, the lanes sharing
+// each ring's cells, until the ring's lower bound exceeds the point's runner-up
+// (the per-lane walk of grid_point, made warp-parallel).  No candidate selection
+// over all k per scan unit and no divergent per-lane rings.  Same decision rule
+// as grid_point: the approximate top three (q, index) decide unless the best two
+// are within SEP or the third within Q_TOL of the runner-up; then the reference's
+// exact arithmetic over every visited candidate within the tolerance.
+template <int D>
+__device__ __forceinline__ int ring_size(int r) {
+  if (r == 0) return 1;
+  return D == 2 ? 8 * r : (2 * r + 1) * (2 * r + 1) * (2 * r + 1);
+}
+// cell e of the ring at Chebyshev distance r around cc (-1: outside the grid, or for
+// 3D an interior cell of the enumerated cube)
+template <int D>
+__device__ __forceinline__ int ring_cell(const int* cc, int r, int e, int G) {
+  int i[3] = {cc[0], cc[1], D == 3 ? cc[2] : 0};
+  if (r > 0) {
+    if (D == 2) {
+      const int side = e / (2 * r), off = e - side * 2 * r;
+      if (side == 0) { i[0] = cc[0] - r + off; i[1] = cc[1] - r; }
+      else if (side == 1) { i[0] = cc[0] + r; i[1] = cc[1] - r + off; }
+      else if (side == 2) { i[0] = cc[0] + r - off; i[1] = cc[1] + r; }
+      else { i[0] = cc[0] - r; i[1] = cc[1] + r - off; }
+    } else {
+      const int n = 2 * r + 1;
+      const int a = e / (n * n), b = (e / n) % n, c = e % n;
+      if (a > 0 && a < n - 1 && b > 0 && b < n - 1 && c > 0 && c < n - 1) return -1;
+      i[0] = cc[0] - r + a;
+      i[1] = cc[1] - r + b;
+      i[2] = cc[2] - r + c;
+    }
+  }
+  int cell = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    if (i[j] < 0 || i[j] >= G) return -1;
+    cell = cell * G + i[j];
+  }
+  return cell;
+}
+
+constexpr int WKT = 256;
+
+template <int D, int WM>
+__global__ void __launch_bounds__(WKT) walk_kernel(gp_assign_args p, int wshift, int64_t nregions,
+                                                   const int32_t* __restrict__ scan,
+                                                   const int32_t* __restrict__ olda,
+                                                   const int32_t* __restrict__ runs) {
+  typedef typename std::conditional<WM == GP_W_UNIT, int, long long>::type RunW;
+  __shared__ WarpTab s_tab[WKT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpTab& tab = s_tab[warp];
+  tab_init(tab, lane);
+  const int G = p.grid_n;
+  unsigned long long nq = 0;
+  const int64_t nitems = nregions * WREG;
+  for (int64_t item = (int64_t)blockIdx.x * (WKT / 32) + warp; item < nitems;
+       item += (int64_t)gridDim.x * (WKT / 32)) {
+    const int64_t r = item / WREG;
+    const int v = (int)(item - r * WREG);
+    if (v >= runs[r]) continue;
+    const int64_t slot = r * WREG + v;
+    const int q = scan[slot];
+    double x[D];
+    load_point<D>(p.X, p.ldx, q, x);
+    int cc[3] = {0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int c = (int)floor((x[j] - p.grid_lo[j]) / p.grid_h);
+      cc[j] = c < 0 ? 0 : (c >= G ? G - 1 : c);
+    }
+    double q1 = INFINITY, q2 = INFINITY, q3 = INFINITY;
+    int i1 = 0x7fffffff, i2 = 0x7fffffff;
+    int rlast = 0;
+    for (int rr = 0;; ++rr) {
+      const int nc = ring_size<D>(rr);
+      for (int e = lane; e < nc; e += 32) {
+        const int cell = ring_cell<D>(cc, rr, e, G);
+        if (cell < 0) continue;
+        for (int t = p.grid_start[cell]; t < p.grid_start[cell + 1]; ++t) {
+          const int c = p.grid_items[t];
+          double s2 = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const double dd = x[j] - p.centers[c * D + j];
+            s2 = fma(dd, dd, s2);
+          }
+          top3_add(q1, i1, q2, i2, q3, s2 * p.inv2_hi[c], c);
+          ++nq;
+        }
+      }
+      double m1 = q1, m2 = q2;
+      for (int o = 16; o; o >>= 1) {
+        const double b1 = __shfl_xor_sync(FULL, m1, o);
+        const double b2 = __shfl_xor_sync(FULL, m2, o);
+        two_min_merge(m1, m2, b1, b2);
+      }
+      rlast = rr;
+      bool covered = true;
+#pragma unroll
+      for (int j = 0; j < D; ++j) covered = covered && cc[j] - rr <= 0 && cc[j] + rr >= G - 1;
+      if (covered) break;
+      const double rh = (double)rr * p.grid_h;
+      const double bound = __dmul_rd(__dmul_rd(rh, rh), p.inv2_min) * (1.0 - 1e-9);
+      if (bound > fma(m2, Q_TOL, m2)) break;
+    }
+    // union of the lanes' top-3 lists (every center was evaluated by one lane)
+    for (int o = 16; o; o >>= 1) {
+      const double b1 = __shfl_xor_sync(FULL, q1, o), b2 = __shfl_xor_sync(FULL, q2, o);
+      const double b3 = __shfl_xor_sync(FULL, q3, o);
+      const int j1 = __shfl_xor_sync(FULL, i1, o), j2 = __shfl_xor_sync(FULL, i2, o);
+      top3_add(q1, i1, q2, i2, q3, b1, j1);
+      top3_add(q1, i1, q2, i2, q3, b2, j2);
+      q3 = fmin(q3, b3);
+    }
+    const double thr = fma(q2, Q_TOL, q2);
+    int bi;
+    float bestf, secondf;
+    if (q3 > thr && q2 > fma(q1, SEP, q1)) {
+      bi = i1;
+      bestf = __fmul_ru(__fsqrt_ru(__double2float_ru(q1)), AP_HI_F);
+      secondf = i2 != 0x7fffffff ? __fmul_rd(__fsqrt_rd(__double2float_rd(q2)), AP_LO_F)
+                                 : INFINITY;
+    } else {
+      double best = INFINITY, second = INFINITY;
+      int bix = 0x7fffffff;
+      for (int rr = 0; rr <= rlast; ++rr) {
+        const int nc = ring_size<D>(rr);
+        for (int e = lane; e < nc; e += 32) {
+          const int cell = ring_cell<D>(cc, rr, e, G);
+          if (cell < 0) continue;
+          for (int t = p.grid_start[cell]; t < p.grid_start[cell + 1]; ++t) {
+            const int c = p.grid_items[t];
+            double s2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              const double dd = x[j] - p.centers[c * D + j];
+              s2 = fma(dd, dd, s2);
+            }
+            if (s2 * p.inv2_hi[c] <= thr) {
+              const double dist = effdist_rn<D>(x, p.centers + c * D, p.infl[c], p.order3);
+              const bool win = dist < best || (dist == best && c < bix);
+              second = win ? best : fmin(second, dist);
+              best = win ? dist : best;
+              bix = win ? c : bix;
+            }
+          }
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(FULL, best, o), os = __shfl_xor_sync(FULL, second, o);
+        const int oi = __shfl_xor_sync(FULL, bix, o);
+        const bool mine = best < ob || (best == ob && bix < oi);
+        second = mine ? fmin(second, ob) : fmin(os, best);
+        best = mine ? best : ob;
+        bix = mine ? bix : oi;
+      }
+      bi = bix;
+      bestf = __double2float_ru(best);
+      secondf = __double2float_rd(second);
+    }
+    RunW wv = 0;
+    if (lane == 0) {
+      if (olda[slot] != bi) p.a[q] = bi;
+      store_bounds(p, lb_params(p, r * WREG), q, bi, bestf, secondf);
+      wv = (RunW)weight_units<WM>(p.w, q, wshift);
+    }
+    tab_add(tab, p.block_w, lane, lane == 0, bi, wv);
+  }
+  for (int o = 16; o; o >>= 1) nq += __shfl_xor_sync(FULL, nq, o);
+  if (lane == 0 && nq) atomicAdd(&p.counters[2], nq);
+  tab_flush(tab, p.block_w, lane);
+}
+
 template <int D, int WM>
 __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
                                                    int sreg, const int32_t* __restrict__ scan,
@@ -1265,6 +1442,19 @@ static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout
     const int64_t items = ((nunits << pshift) + (STH / 32) - 1) / (STH / 32);
     gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>(gmax, items));
   };
+  if (a->flags & 2) {   // sparse warm-up round: warp-per-point grid walks
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t items = L.nregions * WREG;
+    const unsigned gw = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((items + (WKT / 32) * 4 - 1) / ((WKT / 32) * 4), (int64_t)sms * 8));
+    if (a->d == 2)
+      walk_kernel<2, WM><<<gw, WKT, 0, s>>>(*a, wshift, L.nregions, scan, olda, runs);
+    else
+      walk_kernel<3, WM><<<gw, WKT, 0, s>>>(*a, wshift, L.nregions, scan, olda, runs);
+    return;
+  }
   unsigned gs;
   int uch, pshift;
   if (a->d == 2) {

@@ -136,6 +136,13 @@ def sample_ranks_device(n: int, seed: int, device, stream) -> torch.Tensor:
     return rank
 
 
+# warm-up samples with at most WALK_RATIO active points per center (and k >=
+# WALK_MIN_K) assign by warp-per-point grid walks instead of per-unit candidate
+# selection over the k centers (GP_WALK_RATIO=0 disables)
+WALK_RATIO = float(os.environ.get("GP_WALK_RATIO", "12"))
+WALK_MIN_K = 256
+
+
 def full_scan_regions(n: int, k: int) -> int:
     """Full-phase scan unit in 256-entry filter regions: about 1/8 of a block's
     points (SFC-compact units whose boxes stay small against a block), 1..32."""
@@ -369,6 +376,7 @@ class DevicePartitioner:
         self.hier = _Hierarchy(self, use_mega=k > 4096) if k > 128 else None
         self.rmaps = None          # region-local lower-bound maps (full phase)
         self.lists_fresh = False   # candidate lists already match the current parameters
+        self.walk = False          # sparse warm-up rounds use the walk kernel (flags bit 1)
         f = N.FoldArgs()
         f.X, f.ldx, f.d, f.k, f.order3 = self.X.data_ptr(), self.ldx, d, k, self.order3
         f.wmode, f.w, f.a = a.wmode, a.w, self.A.data_ptr()
@@ -428,6 +436,18 @@ class DevicePartitioner:
                self.rstate.data_ptr(), self.rpar.data_ptr(), self.mapflag.data_ptr(),
                1 if reset else 0, self.scale_hint, self.sh)
 
+    def _upload_centers(self, centers: np.ndarray):
+        """Stream-ordered async H2D of the next centers through a pinned buffer."""
+        if getattr(self, "cen_h", None) is None:
+            self.cen_h = torch.empty(centers.shape, dtype=torch.float64, pin_memory=True)
+            self.cen_evt = None
+        if self.cen_evt is not None:
+            self.cen_evt.synchronize()
+        self.cen_h.numpy()[:] = centers
+        self.centers_d.copy_(self.cen_h, non_blocking=True)
+        self.cen_evt = torch.cuda.Event()
+        self.cen_evt.record(self.stream)
+
     def _build_grid(self, centers: np.ndarray):
         """Uniform grid over the point box holding the centers (k-sized host numpy),
         walked by scan units whose candidate set overflows (gp_assign_args.grid_*)."""
@@ -441,11 +461,25 @@ class DevicePartitioner:
         flat = cell[:, 0]
         for j in range(1, d):
             flat = flat * G + cell[:, j]
-        items = np.argsort(flat, kind="stable").astype(np.int32)
-        start = np.zeros(G ** d + 1, dtype=np.int32)
-        np.cumsum(np.bincount(flat, minlength=G ** d), out=start[1:])
-        self.grid_start = torch.from_numpy(start).to(self.device)
-        self.grid_items = torch.from_numpy(items).to(self.device)
+        ncell = G ** d
+        # pinned staging and stream-ordered async uploads (no host-device sync); a
+        # staging buffer is reused only after the copy that read it has completed
+        if getattr(self, "grid_cap", (0, 0)) != (ncell, k):
+            self.grid_cap = (ncell, k)
+            self.grid_h = torch.empty(ncell + 1 + k, dtype=torch.int32, pin_memory=True)
+            self.grid_dev = torch.empty(ncell + 1 + k, dtype=torch.int32, device=self.device)
+            self.grid_evt = None
+        if self.grid_evt is not None:
+            self.grid_evt.synchronize()
+        hv = self.grid_h.numpy()
+        hv[0] = 0
+        np.cumsum(np.bincount(flat, minlength=ncell), out=hv[1:ncell + 1])
+        hv[ncell + 1:] = np.argsort(flat, kind="stable")
+        self.grid_dev.copy_(self.grid_h, non_blocking=True)
+        self.grid_evt = torch.cuda.Event()
+        self.grid_evt.record(self.stream)
+        self.grid_start = self.grid_dev[:ncell + 1]
+        self.grid_items = self.grid_dev[ncell + 1:]
         a = self.aargs
         a.grid_n, a.grid_h = G, h
         a.grid_start, a.grid_items = self.grid_start.data_ptr(), self.grid_items.data_ptr()
@@ -458,6 +492,16 @@ class DevicePartitioner:
         dense = size is not None and self.wplan.exact
         if dense:
             self._enter_dense(m)
+        # sparse warm-up samples (few points per center): warp-per-point grid walks
+        # (gp_assign_args.flags bit 1) need no candidate lists, unit boxes or region maps
+        a = self.aargs
+        k = self.settings.k
+        # decided on the global sample size, so every rank of a sharded run agrees
+        self.walk = (size is not None and a.grid_n > 0 and k >= WALK_MIN_K
+                     and size <= WALK_RATIO * k)
+        a.flags = (a.flags & ~2) | (2 if self.walk else 0)
+        if self.walk:
+            return m
         if self.hier is not None:
             self.hier.prepare(self.aargs.list, m)
         self._unit_boxes(m)
@@ -559,7 +603,7 @@ class DevicePartitioner:
         return m
 
     def _assign(self):
-        if self.hier is not None and not self.lists_fresh:
+        if self.hier is not None and not self.lists_fresh and not self.walk:
             self.hier.refresh()
         self.lists_fresh = False
         self.red.zero_()
@@ -711,7 +755,7 @@ class DevicePartitioner:
             centers = new_centers
             infl = nxt
             last_move = moves
-            self.centers_d.copy_(torch.from_numpy(np.ascontiguousarray(centers)))
+            self._upload_centers(centers)
             self._build_grid(centers)
             self._set_influence(infl, moves=moves)
             if int(self.mapflag.item()):
