@@ -139,7 +139,7 @@ def sample_ranks_device(n: int, seed: int, device, stream) -> torch.Tensor:
 # warm-up samples with at most WALK_RATIO active points per center (and k >=
 # WALK_MIN_K) assign by warp-per-point grid walks instead of per-unit candidate
 # selection over the k centers (GP_WALK_RATIO=0 disables)
-WALK_RATIO = float(os.environ.get("GP_WALK_RATIO", "12"))
+WALK_RATIO = float(os.environ.get("GP_WALK_RATIO", "32"))
 WALK_MIN_K = 256
 
 
