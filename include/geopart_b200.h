@@ -97,14 +97,14 @@ int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx
 
 /* Dense view of a sample phase's active entries (the ~20 balance rounds of one
  * movement iteration then stream contiguous arrays instead of gathering through
- * the active list): gp_gather_state copies A, UBLB (float pairs), X (AoS, d
+ * the active list): gp_gather_state copies A, UBLB (4-byte bound pairs), X (AoS, d
  * columns) and W (wbytes per point, 0 = none) of list[0..m) into dense arrays;
  * gp_scatter_state writes A and UBLB back. */
-int gp_gather_state(const int32_t* list, int64_t m, int d, const int32_t* a, const float* ublb,
-                    const double* X, const void* w, int wbytes, int32_t* a_out, float* ublb_out,
+int gp_gather_state(const int32_t* list, int64_t m, int d, const int32_t* a, const void* ublb,
+                    const double* X, const void* w, int wbytes, int32_t* a_out, void* ublb_out,
                     double* X_out, void* w_out, void* stream);
 int gp_scatter_state(const int32_t* list, int64_t m, const int32_t* a_dense,
-                     const float* ublb_dense, int32_t* a, float* ublb, void* stream);
+                     const void* ublb_dense, int32_t* a, void* ublb, void* stream);
 
 /* K5b warm-up sample order, bit-exact with numpy: rank[perm[t]] = t for
  * perm = numpy.random.default_rng(seed).permutation(n) (kmeans.py:564-567).
@@ -134,8 +134,9 @@ typedef struct gp_assign_args {
   const int32_t* list;    /* active positions (NULL: all positions 0..m-1) */
   int64_t m;              /* number of active entries */
   int32_t* a;             /* assignment per position (-1 = unassigned) */
-  float* ublb;            /* per position (ub~, lb~): normalised bounds, float32 rounded
-                             outward (ub~ up, lb~ down) */
+  void* ublb;             /* per position (ub~, lb~) * bound_scale: normalised bounds as
+                             an IEEE fp16 pair (4 bytes), rounded outward (ub~ up,
+                             lb~ down) */
   const double* centers;  /* k x d row-major */
   const double* infl;     /* k influences */
   const double* inv2_lo;  /* k: lower bound of 1/infl^2 (outward-rounded on the host) */
@@ -188,7 +189,9 @@ typedef struct gp_assign_args {
    * lb_rpar[li >> lb_rshift] instead of lb_par; NULL: the global lb_par */
   const float* lb_rpar;
   int32_t lb_rshift;
-  int32_t pad2;
+  /* power of two applied to the stored fp16 bounds (keeps them in fp16's normal range;
+   * about 1 / the box diagonal) */
+  float bound_scale;
 } gp_assign_args;
 int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);

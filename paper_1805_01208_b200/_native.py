@@ -34,7 +34,7 @@ class AssignArgs(C.Structure):
         ("workspace", vp), ("workspace_bytes", sz), ("scan_regions", i32), ("grid_n", i32),
         ("grid_start", vp), ("grid_items", vp), ("grid_lo", f64 * 3), ("grid_h", f64),
         ("inv2_min", f64), ("unit_boxes", vp), ("unit_shift", i32), ("flags", i32),
-        ("lb_rpar", vp), ("lb_rshift", i32), ("pad2", i32),
+        ("lb_rpar", vp), ("lb_rshift", i32), ("bound_scale", C.c_float),
     ]
 
 

@@ -63,7 +63,8 @@ __device__ __forceinline__ void box_bounds_sq(const double* c, const double* lo,
 __device__ __forceinline__ void store_bounds(const gp_assign_args& p, const float4& L, int64_t q,
                                              int c, float b_up, float s_dn) {
   const float4 N = reinterpret_cast<const float4*>(p.ub_norm)[c];
-  reinterpret_cast<float2*>(p.ublb)[q] = make_float2(ub_normf(N, b_up), lb_normf(L.z, L.w, s_dn));
+  reinterpret_cast<unsigned*>(p.ublb)[q] =
+      bnd_pack(ub_normf(N, b_up), lb_normf(L.z, L.w, s_dn), p.bound_scale);
 }
 
 // lower-bound map parameters (A_lo, B_hi, 1/A_lo, B_lo) of active entry li: its
@@ -183,7 +184,7 @@ static AssignLayout assign_layout(int64_t m) {
 // completion on the stage's mbarrier), so each warp's HBM stream runs ahead of it
 // with no CTA-wide barrier; other regions (sparse lists, the tail) use direct loads.
 constexpr int FSTAGES = 2;
-constexpr int FREG_BYTES = WREG * 12;   // a (4 B) + (ub, lb) (8 B) per entry
+constexpr int FREG_BYTES = WREG * 8;    // a (4 B) + packed (ub, lb) (4 B) per entry
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -240,7 +241,8 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
     unsigned char* base = wsm + (size_t)sg * FREG_BYTES;
     mbar_expect_tx(&s_bar[warp][sg], FREG_BYTES);
     bulk_g2s(base, p.a + e0, WREG * 4, &s_bar[warp][sg]);
-    bulk_g2s(base + WREG * 4, p.ublb + 2 * e0, WREG * 8, &s_bar[warp][sg]);
+    bulk_g2s(base + WREG * 4, reinterpret_cast<const unsigned*>(p.ublb) + e0, WREG * 4,
+             &s_bar[warp][sg]);
   };
   if (lane == 0) {
     for (int sg = 0; sg < FSTAGES; ++sg) mbar_init(&s_bar[warp][sg], 1);
@@ -249,6 +251,7 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
   }
   __syncwarp();
   unsigned long long nskip = 0;
+  const float binv = __frcp_rn(p.bound_scale);   // exact: a power of two
   int st = 0;            // ring stage of the next staged region, and its use parity
   unsigned phase = 0;
   for (int64_t c = cb; c < ce; ++c) {
@@ -263,14 +266,15 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
       mbar_wait(&s_bar[warp][st], phase);
       const unsigned char* base = wsm + (size_t)st * FREG_BYTES;
       const int2* as = reinterpret_cast<const int2*>(base);
-      const float4* bs = reinterpret_cast<const float4*>(base + WREG * 4);
+      const uint2* bs = reinterpret_cast<const uint2*>(base + WREG * 4);
 #pragma unroll
       for (int h = 0; h < FPER / 2; ++h) {
         const int2 av = as[h * 32 + lane];
-        const float4 bv = bs[h * 32 + lane];
+        const uint2 bw = bs[h * 32 + lane];
+        const float2 b0 = bnd_unpack(bw.x, binv), b1 = bnd_unpack(bw.y, binv);
         a[2 * h] = av.x; a[2 * h + 1] = av.y;
-        ub[2 * h] = bv.x; lb[2 * h] = bv.y;
-        ub[2 * h + 1] = bv.z; lb[2 * h + 1] = bv.w;
+        ub[2 * h] = b0.x; lb[2 * h] = b0.y;
+        ub[2 * h + 1] = b1.x; lb[2 * h + 1] = b1.y;
         q[2 * h] = rbase + 64 * h;
         q[2 * h + 1] = rbase + 64 * h + 1;
       }
@@ -291,8 +295,9 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
         q[e] = li < p.m ? (p.list ? p.list[li] : li) : -1;
         nvalid += q[e] >= 0;
         a[e] = q[e] >= 0 ? p.a[q[e]] : -1;
-        const float2 v = q[e] >= 0 ? reinterpret_cast<const float2*>(p.ublb)[q[e]]
-                                   : make_float2(0.f, 0.f);
+        const float2 v = q[e] >= 0
+                             ? bnd_unpack(reinterpret_cast<const unsigned*>(p.ublb)[q[e]], binv)
+                             : make_float2(0.f, 0.f);
         ub[e] = v.x;
         lb[e] = v.y;
       }
@@ -1062,7 +1067,8 @@ __global__ void audit_kernel(gp_assign_args p, unsigned long long* out) {
     double x[D];
     load_point<D>(p.X, p.ldx, q, x);
     const int a = p.a[q];
-    const float2 bnd = reinterpret_cast<const float2*>(p.ublb)[q];
+    const float2 bnd =
+        bnd_unpack(reinterpret_cast<const unsigned*>(p.ublb)[q], __frcp_rn(p.bound_scale));
     double m1 = INFINITY, m2 = INFINITY, own = 0.0;
     int arg = 0;
     for (int c = 0; c < p.k; ++c) {
@@ -1100,7 +1106,8 @@ __global__ void lb_remap_kernel(gp_assign_args p, int mode) {
   for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < p.m;
        li += (int64_t)gridDim.x * blockDim.x) {
     const int q = p.list ? p.list[li] : (int)li;
-    float2 bnd = reinterpret_cast<const float2*>(p.ublb)[q];
+    float2 bnd =
+        bnd_unpack(reinterpret_cast<const unsigned*>(p.ublb)[q], __frcp_rn(p.bound_scale));
     const float4 G = *reinterpret_cast<const float4*>(p.lb_par);
     if (mode == 0) {
       bnd.y = lb_evalf(G.x, bnd.y, G.y);
@@ -1108,7 +1115,7 @@ __global__ void lb_remap_kernel(gp_assign_args p, int mode) {
       const float4 L = reinterpret_cast<const float4*>(p.lb_rpar)[li >> p.lb_rshift];
       bnd.y = lb_normf(G.z, G.w, lb_evalf(L.x, bnd.y, L.y));
     }
-    reinterpret_cast<float2*>(p.ublb)[q] = bnd;
+    reinterpret_cast<unsigned*>(p.ublb)[q] = bnd_pack(bnd.x, bnd.y, p.bound_scale);
   }
 }
 
@@ -1117,12 +1124,13 @@ __global__ void rebase_kernel(gp_assign_args p) {
        li += (int64_t)gridDim.x * blockDim.x) {
     const int q = p.list ? p.list[li] : (int)li;
     const int a = p.a[q];
-    const float2 bnd = reinterpret_cast<const float2*>(p.ublb)[q];
+    const float2 bnd =
+        bnd_unpack(reinterpret_cast<const unsigned*>(p.ublb)[q], __frcp_rn(p.bound_scale));
     // the host resets the maps to identity after this pass: store the values themselves
     const float ub = a >= 0 ? ub_evalf(reinterpret_cast<const float4*>(p.ub_eval)[a], bnd.x)
                             : bnd.x;
     const float4 L = lb_params(p, li);
-    reinterpret_cast<float2*>(p.ublb)[q] = make_float2(ub, lb_evalf(L.x, bnd.y, L.y));
+    reinterpret_cast<unsigned*>(p.ublb)[q] = bnd_pack(ub, lb_evalf(L.x, bnd.y, L.y), p.bound_scale);
   }
 }
 
@@ -1392,6 +1400,7 @@ static int validate(const gp_assign_args* a) {
   GP_REQUIRE(a->wmode == GP_W_UNIT || a->w != nullptr, "weights missing");
   GP_REQUIRE(a->inv2_lo && a->inv2_hi, "inv2 bounds missing");
   GP_REQUIRE(a->ub_eval && a->ub_norm && a->lb_par, "bound maps missing");
+  GP_REQUIRE(a->bound_scale > 0.f, "bound_scale must be a positive power of two");
   return GP_OK;
 }
 

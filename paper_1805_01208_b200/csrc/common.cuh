@@ -8,6 +8,7 @@
 // they stay rigorous.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -91,6 +92,20 @@ __device__ __forceinline__ float ub_normf(float4 N, float b_up) {
 __device__ __forceinline__ float lb_normf(float inva, float blo, float s_dn) {
   if (isinf(s_dn)) return s_dn;
   return __fmul_rd(__fadd_rd(s_dn, blo), inva);
+}
+
+// Stored bounds: (ub~, lb~) times the power of two `scale` as an fp16 pair, ub~
+// rounded up and lb~ rounded down (4 bytes per point).  Unpacking
+// multiplies by 1/scale, exact for a power of two.
+__device__ __forceinline__ unsigned bnd_pack(float u, float l, float scale) {
+  const __half hu = __float2half_ru(u * scale);
+  const __half hl = __float2half_rd(l * scale);
+  return (unsigned)__half_as_ushort(hu) | ((unsigned)__half_as_ushort(hl) << 16);
+}
+__device__ __forceinline__ float2 bnd_unpack(unsigned w, float inv_scale) {
+  const float u = __half2float(__ushort_as_half((unsigned short)(w & 0xffffu)));
+  const float l = __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+  return make_float2(u * inv_scale, l * inv_scale);
 }
 
 // point i of an AoS coordinate array with point stride ldx

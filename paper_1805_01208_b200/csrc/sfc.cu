@@ -263,10 +263,10 @@ __global__ void gather_ranks_kernel(const int32_t* __restrict__ r, const uint32_
 }
 
 __global__ void gather_state_kernel(const int32_t* __restrict__ list, int64_t m, int d,
-                                    const int32_t* __restrict__ a, const float2* __restrict__ ublb,
+                                    const int32_t* __restrict__ a, const uint32_t* __restrict__ ublb,
                                     const double* __restrict__ X, const uint8_t* __restrict__ w,
                                     int wbytes, int32_t* __restrict__ a_out,
-                                    float2* __restrict__ ublb_out, double* __restrict__ X_out,
+                                    uint32_t* __restrict__ ublb_out, double* __restrict__ X_out,
                                     uint8_t* __restrict__ w_out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -282,8 +282,8 @@ __global__ void gather_state_kernel(const int32_t* __restrict__ list, int64_t m,
 
 __global__ void scatter_state_kernel(const int32_t* __restrict__ list, int64_t m,
                                      const int32_t* __restrict__ a_dense,
-                                     const float2* __restrict__ ublb_dense, int32_t* __restrict__ a,
-                                     float2* __restrict__ ublb) {
+                                     const uint32_t* __restrict__ ublb_dense, int32_t* __restrict__ a,
+                                     uint32_t* __restrict__ ublb) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = list[i];
@@ -444,23 +444,23 @@ int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx
   return check_launch("compact_active");
 }
 
-int gp_gather_state(const int32_t* list, int64_t m, int d, const int32_t* a, const float* ublb,
-                    const double* X, const void* w, int wbytes, int32_t* a_out, float* ublb_out,
+int gp_gather_state(const int32_t* list, int64_t m, int d, const int32_t* a, const void* ublb,
+                    const double* X, const void* w, int wbytes, int32_t* a_out, void* ublb_out,
                     double* X_out, void* w_out, void* stream) {
   GP_REQUIRE(d == 2 || d == 3, "gp_gather_state: bad d");
   GP_REQUIRE(wbytes == 0 || wbytes == 4 || wbytes == 8, "gp_gather_state: bad wbytes");
   if (m == 0) return GP_OK;
   gather_state_kernel<<<stride_grid(m), 256, 0, (cudaStream_t)stream>>>(
-      list, m, d, a, (const float2*)ublb, X, (const uint8_t*)w, wbytes, a_out, (float2*)ublb_out,
+      list, m, d, a, (const uint32_t*)ublb, X, (const uint8_t*)w, wbytes, a_out, (uint32_t*)ublb_out,
       X_out, (uint8_t*)w_out);
   return check_launch("gather_state");
 }
 
 int gp_scatter_state(const int32_t* list, int64_t m, const int32_t* a_dense,
-                     const float* ublb_dense, int32_t* a, float* ublb, void* stream) {
+                     const void* ublb_dense, int32_t* a, void* ublb, void* stream) {
   if (m == 0) return GP_OK;
   scatter_state_kernel<<<stride_grid(m), 256, 0, (cudaStream_t)stream>>>(
-      list, m, a_dense, (const float2*)ublb_dense, a, (float2*)ublb);
+      list, m, a_dense, (const uint32_t*)ublb_dense, a, (uint32_t*)ublb);
   return check_launch("scatter_state");
 }
 

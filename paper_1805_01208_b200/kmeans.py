@@ -335,8 +335,9 @@ class DevicePartitioner:
     def _alloc_state(self):
         n, k, d, dev = self.n, self.settings.k, self.d, self.device
         self.A = torch.full((n,), -1, dtype=torch.int32, device=dev)
-        # (ub~, lb~) float32 pairs: ub~ = +inf (unassigned), lb~ = 0 (kmeans.py:146-147)
-        self.UBLB = torch.zeros((n, 2), dtype=torch.float32, device=dev)
+        # (ub~, lb~) fp16 pairs (scaled by bound_scale): ub~ = +inf (unassigned), lb~ = 0
+        # (kmeans.py:146-147)
+        self.UBLB = torch.zeros((n, 2), dtype=torch.float16, device=dev)
         self.UBLB[:, 0] = math.inf
         # influences (ping-pong) | inv2_lo | inv2_hi | moves   (float64)
         self.kstate = torch.empty(5 * k, dtype=torch.float64, device=dev)
@@ -360,6 +361,9 @@ class DevicePartitioner:
         a.w = _ptr(self.W)
         a.wscale = self.wplan.scale
         a.a, a.ublb = self.A.data_ptr(), self.UBLB.data_ptr()
+        # stored bounds are fp16 times a power of two near 1 / the box diagonal
+        e = -int(round(math.log2(max(self.box.diagonal(), 1e-30))))
+        a.bound_scale = 2.0 ** max(-60, min(60, e))
         a.centers = self.centers_d.data_ptr()
         base = self.kstate.data_ptr()
         a.infl, a.inv2_lo, a.inv2_hi = base, base + 16 * k, base + 24 * k
@@ -554,7 +558,7 @@ class DevicePartitioner:
             cap = max(self.sizes)
             self.dense_cap = cap
             self.A_d = torch.empty(cap, dtype=torch.int32, device=dev)
-            self.UBLB_d = torch.empty((cap, 2), dtype=torch.float32, device=dev)
+            self.UBLB_d = torch.empty((cap, 2), dtype=torch.float16, device=dev)
             self.X_d = torch.empty((cap, d), dtype=torch.float64, device=dev)
             self.W_d = None if self.W is None else torch.empty(cap, dtype=self.W.dtype, device=dev)
         wbytes = 0 if self.W is None else self.W.element_size()
