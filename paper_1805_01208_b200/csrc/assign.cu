@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
   for (int64_t c = cb; c < ce; ++c) {
     const int reg = (int)c * (FCHUNK / WREG) + warp;   // m < 2^31: 32-bit entry math
     const int rbase = reg * WREG + 2 * lane;
-    const float4 lbp = lb_params(p, (int64_t)reg * WREG);   // one map per 2^15 entries
+    float4 lbp = lb_params(p, (int64_t)reg * WREG);   // one map per 2^15 entries
+    lbp.x *= binv;                                     // slope on the scaled stored lb~
     int a[FPER], q[FPER];
     float ub[FPER], lb[FPER];
     const bool staged = c < fe;
@@ -271,7 +272,8 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
       for (int h = 0; h < FPER / 2; ++h) {
         const int2 av = as[h * 32 + lane];
         const uint2 bw = bs[h * 32 + lane];
-        const float2 b0 = bnd_unpack(bw.x, binv), b1 = bnd_unpack(bw.y, binv);
+        // raw scaled values: the bound-map slopes below carry the 1/bound_scale factor
+        const float2 b0 = bnd_raw(bw.x), b1 = bnd_raw(bw.y);
         a[2 * h] = av.x; a[2 * h + 1] = av.y;
         ub[2 * h] = b0.x; lb[2 * h] = b0.y;
         ub[2 * h + 1] = b1.x; lb[2 * h + 1] = b1.y;
@@ -295,9 +297,8 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
         q[e] = li < p.m ? (p.list ? p.list[li] : li) : -1;
         nvalid += q[e] >= 0;
         a[e] = q[e] >= 0 ? p.a[q[e]] : -1;
-        const float2 v = q[e] >= 0
-                             ? bnd_unpack(reinterpret_cast<const unsigned*>(p.ublb)[q[e]], binv)
-                             : make_float2(0.f, 0.f);
+        const float2 v = q[e] >= 0 ? bnd_raw(reinterpret_cast<const unsigned*>(p.ublb)[q[e]])
+                                   : make_float2(0.f, 0.f);
         ub[e] = v.x;
         lb[e] = v.y;
       }
@@ -313,7 +314,9 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
 #pragma unroll
     for (int e = 1; e < FPER; ++e) same = same && a[e] == a[0];
     if (same) {
-      const float4 E = reinterpret_cast<const float4*>(p.ub_eval)[a[0]];
+      float4 E = reinterpret_cast<const float4*>(p.ub_eval)[a[0]];
+      E.x *= binv;   // exact: the stored ub~ carries bound_scale
+      E.y *= binv;
       unsigned keep = 0;
 #pragma unroll
       for (int e = 0; e < FPER; ++e) {
@@ -341,6 +344,8 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
         const int ae = a[e];
         if (ae >= 0 && ae != ea) {
           E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
+          E.x *= binv;
+          E.y *= binv;
           ea = ae;
         }
         const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);

@@ -108,6 +108,12 @@ __device__ __forceinline__ float2 bnd_unpack(unsigned w, float inv_scale) {
   return make_float2(u * inv_scale, l * inv_scale);
 }
 
+// the stored pair as floats, still multiplied by the scale (the filter folds
+// 1/scale into the bound-map slopes: exact for a power of two)
+__device__ __forceinline__ float2 bnd_raw(unsigned w) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+
 // point i of an AoS coordinate array with point stride ldx
 template <int D>
 __device__ __forceinline__ void load_point(const double* X, int64_t ldx, int64_t i, double* out) {
