@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t*
   __shared__ double scen[W][G][D];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t P = counters[3];
-  int pair = -1, j = 0, j1 = 0, cur = 0, re = 0;
+  // (ns, ne): bounds of run j + 1 and rn2 = sidx[j + 2], prefetched one run ahead so
+  // that a run change needs no dependent loads on the step's critical path
+  int pair = -1, j = 0, j1 = 0, cur = 0, re = 0, ns = 0, ne = 0, rn2 = 0;
   auto fetch = [&]() {
     const int64_t pi = (int64_t)atomicAdd((unsigned long long*)&counters[1], 1ull);
     if (pi >= P) {
@@ -267,6 +269,12 @@ __global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t*
     const int r = sidx[j];
     cur = starts[r];
     re = starts[r + 1];
+    if (j + 1 < j1) {
+      const int r1 = sidx[j + 1];
+      ns = starts[r1];
+      ne = starts[r1 + 1];
+    }
+    if (j + 2 < j1) rn2 = sidx[j + 2];
     if (NC > 1) {
       const int c = (int)(skey[j] & ((1u << block_bits(f.k)) - 1));
 #pragma unroll
@@ -341,9 +349,13 @@ __global__ void __launch_bounds__(FT) fold_groups(gp_fold_args f, const int32_t*
       if (cur >= re) {
         ++j;
         if (j < j1) {
-          const int r = sidx[j];
-          cur = starts[r];
-          re = starts[r + 1];
+          cur = ns;
+          re = ne;
+          if (j + 1 < j1) {
+            ns = starts[rn2];
+            ne = starts[rn2 + 1];
+            if (j + 2 < j1) rn2 = sidx[j + 2];
+          }
         } else {
           done = true;
         }
