@@ -23,6 +23,8 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gp {
@@ -615,7 +617,16 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
       else GP_FOLD(3, 1, 1, 8);
     }
   } else if (f->d == 2) {
-    if (per >= 8) GP_FOLD(2, 4, 8, 1);
+    static int shape = -1;   // GP_FOLD_SHAPE=G (1, 2, 4, 8) overrides the choice (tuning)
+    if (shape < 0) {
+      const char* e = getenv("GP_FOLD_SHAPE");
+      shape = e ? atoi(e) : 0;
+    }
+    if (shape == 8) GP_FOLD(2, 4, 8, 1);
+    else if (shape == 4) GP_FOLD(2, 4, 4, 2);
+    else if (shape == 2) GP_FOLD(2, 4, 2, 4);
+    else if (shape == 1) GP_FOLD(2, 4, 1, 8);
+    else if (per >= 8) GP_FOLD(2, 4, 8, 1);
     else if (per >= 4) GP_FOLD(2, 4, 4, 2);
     else if (per >= 2) GP_FOLD(2, 4, 2, 4);
     else GP_FOLD(2, 4, 1, 8);

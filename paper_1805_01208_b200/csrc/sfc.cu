@@ -185,16 +185,42 @@ __global__ void hilbert_kernel(const double* __restrict__ pts, int64_t n, int64_
 }
 
 // ---------------------------------------------------------- payload gather
+// Four independent elements per thread and iteration: the random reads of a
+// thread (gids, then the points) are all in flight together.
 __global__ void gather_points_kernel(const double* __restrict__ pts, int64_t sp, int64_t sd, int d,
                                      const uint32_t* __restrict__ gids, int64_t n,
                                      double* __restrict__ X, int64_t ldx,
                                      const double* __restrict__ w_in, int wmode, void* w_out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t g = gids[i];
-    for (int j = 0; j < d; ++j) X[i * ldx + j] = pts[g * sp + j * sd];
-    if (wmode == GP_W_F32) ((float*)w_out)[i] = (float)w_in[g];
-    else if (wmode == GP_W_F64) ((double*)w_out)[i] = w_in[g];
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    int64_t g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      g[u] = i < n ? (int64_t)gids[i] : 0;
+    }
+    double v[U][3];
+    double wv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) v[u][j] = (i < n && j < d) ? pts[g[u] * sp + j * sd] : 0.0;
+      wv[u] = (i < n && wmode != GP_W_UNIT) ? w_in[g[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= n) continue;
+      if (d == 2 && ldx == 2) {
+        reinterpret_cast<double2*>(X)[i] = make_double2(v[u][0], v[u][1]);
+      } else {
+        for (int j = 0; j < d; ++j) X[i * ldx + j] = v[u][j];
+      }
+      if (wmode == GP_W_F32) ((float*)w_out)[i] = (float)wv[u];
+      else if (wmode == GP_W_F64) ((double*)w_out)[i] = wv[u];
+    }
   }
 }
 
@@ -257,9 +283,19 @@ __global__ void scatter_gid_kernel(const int32_t* __restrict__ a, const uint32_t
 
 __global__ void gather_ranks_kernel(const int32_t* __restrict__ r, const uint32_t* __restrict__ g,
                                     int64_t n, int32_t* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = r[g[i]];
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    uint32_t gg[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) gg[u] = i0 + u * stride < n ? g[i0 + u * stride] : 0u;
+    int32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = i0 + u * stride < n ? r[gg[u]] : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < n) out[i0 + u * stride] = v[u];
+  }
 }
 
 __global__ void gather_state_kernel(const int32_t* __restrict__ list, int64_t m, int d,
