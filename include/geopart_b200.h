@@ -218,8 +218,9 @@ int gp_group_candidates(const double* boxes, int64_t ngroups, int d, int k,
 
 /* Device-side bound-map bookkeeping (control.BoundMaps on the GPU): compose one
  * relaxation (kmeans.py:208-239) old_infl -> new_infl with center moves `moves`
- * (NULL = zero moves) into the cumulative maps `state` (S[k], T[k], then A, B,
- * steps as doubles), unless it is the reference's identity early return, and
+ * (NULL = zero moves) into the cumulative maps `state` (4k + 6 doubles: S[k], T[k],
+ * A, B, steps, 3 scratch, then this relaxation's per-cluster ratio I_old/I_new [k]
+ * and shift move/I_new [k]), unless it is the reference's identity early return, and
  * derive every parameter the kernels read: inv2_lo/inv2_hi (k), ub_eval/ub_norm
  * (k x 4 floats), lb_par (4 floats).  flags[0] is set to 1 when the maps should
  * be re-based (gp_rebase_bounds + gp_reset_maps).  reset != 0 starts from
@@ -236,6 +237,8 @@ int gp_update_maps(const double* old_infl, const double* new_infl, const double*
  * and influences) can be the nearest or the runner-up: every other center is
  * farther than the group's second-smallest upper bound, which bounds the
  * runner-up of every entry.  So the relaxation over the list alone is sound.
+ * map_state: the state of the gp_update_maps call for the same relaxation (its
+ * per-cluster ratios and shifts are gathered over the lists).
  * rstate: nregions x 3 doubles (A, B, steps); rpar: nregions x float4 in the
  * layout of lb_par.  reset = 1: identity maps.  flags[0] = 1 when a map leaves
  * the float32 range (the caller rebases). */
@@ -244,10 +247,9 @@ int gp_update_maps(const double* old_infl, const double* new_infl, const double*
  * them from the region maps (lb_rpar) to the global map. */
 int gp_lb_remap(const gp_assign_args* args, int mode, void* stream);
 
-int gp_region_maps(const double* old_infl, const double* new_infl, const double* moves, int k,
-                   const int32_t* group_list, const int32_t* group_count, int group_cap,
-                   int64_t nregions, double* rstate, float* rpar, int32_t* flags, int reset,
-                   double scale_hint, void* stream);
+int gp_region_maps(const double* map_state, int k, const int32_t* group_list,
+                   const int32_t* group_count, int group_cap, int64_t nregions, double* rstate,
+                   float* rpar, int32_t* flags, int reset, double scale_hint, void* stream);
 
 /* Re-express every bound under identity maps (when the host's cumulative
  * maps drift out of range).  Same bound semantics as gp_assign_args. */

@@ -77,8 +77,8 @@ _SIGS = {
     "gp_movement_fold": (C.c_int, [C.POINTER(FoldArgs), vp]),
     "gp_fold_stats": (C.c_int, [vp]),
     "gp_lb_remap": (C.c_int, [vp, C.c_int, vp]),
-    "gp_region_maps": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, C.c_int, i64, vp, vp, vp, C.c_int,
-                                 f64, vp]),
+    "gp_region_maps": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, i64, vp, vp, vp, C.c_int, f64,
+                                 vp]),
     "gp_scan_stats": (C.c_int, [vp, C.c_int]),
     "gp_fold_export": (C.c_int, [C.POINTER(FoldArgs), vp, vp, vp, vp]),
     "gp_fold_combine_bytes": (C.c_int, [C.c_int, C.POINTER(sz)]),
@@ -130,7 +130,7 @@ KERNELS_PER_CALL = {
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 4,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
-    "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 1, "gp_region_maps": 1, "gp_lb_remap": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
+    "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 3, "gp_region_maps": 1, "gp_lb_remap": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
     "gp_sfc_cut": 3, "gp_predict": 1,
 }
 _launches = [0]

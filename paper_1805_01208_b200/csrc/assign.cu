@@ -1257,59 +1257,54 @@ __global__ void __launch_bounds__(256) group_candidates_kernel(
 // Mirror of control.BoundMaps.relax + device_params for one CTA.
 constexpr double UBS = 1.0 + 1e-12, LBS = 1.0 - 1e-12;
 
-__global__ void __launch_bounds__(1024) update_maps_kernel(
-    const double* __restrict__ old_infl, const double* __restrict__ new_infl,
-    const double* __restrict__ moves, int k, double* __restrict__ st,
-    double* __restrict__ inv2_lo, double* __restrict__ inv2_hi, float4* __restrict__ ub_eval,
-    float4* __restrict__ ub_norm, float* __restrict__ lb_par, int32_t* __restrict__ flags,
-    int reset, double scale_hint) {
-  __shared__ double s_min[32], s_max[32];
-  __shared__ int s_any[32];
-  double* S = st;
-  double* T = st + k;
-  double* ABs = st + 2 * k;  // A, B, steps
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // reductions: changed?, min ratio, max shift
+// gp_update_maps in three steps over many CTAs (it used to be one 1024-thread CTA,
+// ~50 us per round at k = 16384):
+//  1. maps_ratio_kernel: per cluster ratio = I_old/I_new and shift = move/I_new
+//     (kept for gp_region_maps) and the global min ratio, max shift and "anything
+//     changed" as order-preserving atomics (both are >= 0);
+//  2. maps_global_kernel (one thread): the lower-bound map A, B, steps and lb_par;
+//  3. maps_cluster_kernel: the per-cluster maps and parameters.
+// state layout: S[k] | T[k] | A, B, steps | rmin, smax, any (scratch) | ratio[k] | shift[k]
+__global__ void maps_ratio_kernel(const double* __restrict__ old_infl,
+                                  const double* __restrict__ new_infl,
+                                  const double* __restrict__ moves, int k,
+                                  double* __restrict__ st) {
+  double* scr = st + 2 * k + 3;
+  double* ratio = st + 2 * k + 6;
+  double* shift = ratio + k;
   double rmin = INFINITY, smax = 0.0;
   int any = 0;
-  for (int c = tid; c < k; c += blockDim.x) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
     const double mv = moves ? moves[c] : 0.0;
     any |= (mv != 0.0) || (old_infl[c] != new_infl[c]);
-    rmin = fmin(rmin, old_infl[c] / new_infl[c]);
-    smax = fmax(smax, mv / new_infl[c]);
+    const double r = old_infl[c] / new_infl[c];
+    const double sh = mv / new_infl[c];
+    ratio[c] = r;
+    shift[c] = sh;
+    rmin = fmin(rmin, r);
+    smax = fmax(smax, sh);
   }
   for (int o = 16; o; o >>= 1) {
     rmin = fmin(rmin, __shfl_xor_sync(FULL, rmin, o));
     smax = fmax(smax, __shfl_xor_sync(FULL, smax, o));
     any |= __shfl_xor_sync(FULL, any, o);
   }
-  if (lane == 0) {
-    s_min[warp] = rmin;
-    s_max[warp] = smax;
-    s_any[warp] = any;
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long* u = reinterpret_cast<unsigned long long*>(scr);
+    atomicMin(&u[0], (unsigned long long)__double_as_longlong(rmin));   // doubles >= 0
+    atomicMax(&u[1], (unsigned long long)__double_as_longlong(smax));
+    if (any) atomicOr(&u[2], 1ull);
   }
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x / 32;
-    rmin = lane < nw ? s_min[lane] : INFINITY;
-    smax = lane < nw ? s_max[lane] : 0.0;
-    any = lane < nw ? s_any[lane] : 0;
-    for (int o = 16; o; o >>= 1) {
-      rmin = fmin(rmin, __shfl_xor_sync(FULL, rmin, o));
-      smax = fmax(smax, __shfl_xor_sync(FULL, smax, o));
-      any |= __shfl_xor_sync(FULL, any, o);
-    }
-    if (lane == 0) {
-      s_min[0] = rmin;
-      s_max[0] = smax;
-      s_any[0] = any;
-    }
-  }
-  __syncthreads();
-  rmin = s_min[0];
-  smax = s_max[0];
+}
+
+__global__ void maps_global_kernel(int k, double* __restrict__ st, float* __restrict__ lb_par,
+                                   int32_t* __restrict__ flags, int reset, double scale_hint) {
+  double* ABs = st + 2 * k;
+  const unsigned long long* u = reinterpret_cast<const unsigned long long*>(st + 2 * k + 3);
+  const double rmin = __longlong_as_double((long long)u[0]);
+  const double smax = __longlong_as_double((long long)u[1]);
   // relax_bounds' identity early return (kmeans.py:223-228)
-  const bool compose = !reset && s_any[0];
+  const bool compose = !reset && u[2] != 0;
   double A = reset ? 1.0 : ABs[0], B = reset ? 0.0 : ABs[1], steps = reset ? 0.0 : ABs[2];
   if (compose) {
     A = A * rmin * LBS;
@@ -1317,14 +1312,36 @@ __global__ void __launch_bounds__(1024) update_maps_kernel(
     steps += 1.0;
   }
   const double e = (4.0 * steps + 16.0) * 0x1p-52;
+  ABs[0] = A;
+  ABs[1] = B;
+  ABs[2] = steps;
+  lb_par[0] = __double2float_rd(__dmul_rd(A, 1.0 - e));
+  lb_par[1] = __double2float_ru(__dmul_ru(B, 1.0 + e));
+  lb_par[2] = __double2float_rd(__ddiv_rd(1.0, A));
+  lb_par[3] = __double2float_rd(B);
+  if (A < 1e-6 || A > 1e6 || B > 64.0 * scale_hint) flags[0] = 1;
+}
+
+__global__ void maps_cluster_kernel(const double* __restrict__ new_infl, int k,
+                                    double* __restrict__ st, double* __restrict__ inv2_lo,
+                                    double* __restrict__ inv2_hi, float4* __restrict__ ub_eval,
+                                    float4* __restrict__ ub_norm, int32_t* __restrict__ flags,
+                                    int reset, double scale_hint) {
+  double* S = st;
+  double* T = st + k;
+  const double steps = st[2 * k + 2];   // already composed by maps_global_kernel
+  const unsigned long long any = reinterpret_cast<const unsigned long long*>(st + 2 * k + 3)[2];
+  const bool compose = !reset && any != 0;
+  const double* ratio = st + 2 * k + 6;
+  const double* shift = ratio + k;
+  const double e = (4.0 * steps + 16.0) * 0x1p-52;
   int out_of_range = 0;
-  for (int c = tid; c < k; c += blockDim.x) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
     double Sc = reset ? 1.0 : S[c], Tc = reset ? 0.0 : T[c];
     if (compose) {
-      const double r = old_infl[c] / new_infl[c];
-      const double sh = (moves ? moves[c] : 0.0) / new_infl[c];
+      const double r = ratio[c];
       Sc = Sc * r * UBS;
-      Tc = (Tc * r + sh) * UBS;
+      Tc = (Tc * r + shift[c]) * UBS;
     }
     S[c] = Sc;
     T[c] = Tc;
@@ -1338,25 +1355,15 @@ __global__ void __launch_bounds__(1024) update_maps_kernel(
                              __double2float_rd(__ddiv_rd(1.0, Sc)), __double2float_rd(Tc), 0.f);
     out_of_range |= Sc < 1e-6 || Sc > 1e6 || Tc > 64.0 * scale_hint;
   }
-  out_of_range = __syncthreads_or(out_of_range);
-  if (tid == 0) {
-    ABs[0] = A;
-    ABs[1] = B;
-    ABs[2] = steps;
-    lb_par[0] = __double2float_rd(__dmul_rd(A, 1.0 - e));
-    lb_par[1] = __double2float_ru(__dmul_ru(B, 1.0 + e));
-    lb_par[2] = __double2float_rd(__ddiv_rd(1.0, A));
-    lb_par[3] = __double2float_rd(B);
-    if (out_of_range || A < 1e-6 || A > 1e6 || B > 64.0 * scale_hint) flags[0] = 1;
-  }
+  if (__any_sync(FULL, out_of_range) && (threadIdx.x & 31) == 0) flags[0] = 1;
 }
 
 // one warp per region: smallest ratio / largest shift over the region's candidate
 // list (all k when the list overflowed), composed into its lower-bound map like
 // update_maps_kernel composes the global one
 __global__ void __launch_bounds__(256) region_maps_kernel(
-    const double* __restrict__ old_infl, const double* __restrict__ new_infl,
-    const double* __restrict__ moves, int k, const int32_t* __restrict__ glist,
+    const double* __restrict__ ratio, const double* __restrict__ shift, int k,
+    const int32_t* __restrict__ glist,
     const int32_t* __restrict__ gcount, int gcap, int64_t R, double* __restrict__ rst,
     float4* __restrict__ rpar, int32_t* __restrict__ flags, int reset, double scale_hint) {
   const int lane = threadIdx.x & 31;
@@ -1370,8 +1377,8 @@ __global__ void __launch_bounds__(256) region_maps_kernel(
     double rmin = INFINITY, smax = 0.0;
     for (int i = lane; i < ns; i += 32) {
       const int c = lst ? lst[i] : i;
-      rmin = fmin(rmin, old_infl[c] / new_infl[c]);
-      smax = fmax(smax, (moves ? moves[c] : 0.0) / new_infl[c]);
+      rmin = fmin(rmin, ratio[c]);
+      smax = fmax(smax, shift[c]);
     }
     for (int o = 16; o; o >>= 1) {
       rmin = fmin(rmin, __shfl_xor_sync(FULL, rmin, o));
@@ -1529,21 +1536,27 @@ int gp_update_maps(const double* old_infl, const double* new_infl, const double*
                    float* ub_norm, float* lb_par, int32_t* flags, int reset, double scale_hint,
                    void* stream) {
   GP_REQUIRE(k >= 1 && old_infl && new_infl && state, "gp_update_maps: bad args");
-  update_maps_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
-      old_infl, new_infl, moves, k, state, inv2_lo, inv2_hi, (float4*)ub_eval, (float4*)ub_norm,
-      lb_par, flags, reset, scale_hint);
+  cudaStream_t s = (cudaStream_t)stream;
+  double* scr = state + 2 * k + 3;
+  GP_CUDA(cudaMemsetAsync(scr, 0xff, sizeof(double), s));            // rmin: +max key
+  GP_CUDA(cudaMemsetAsync(scr + 1, 0, 2 * sizeof(double), s));       // smax, any
+  const unsigned g = grid_for(k, 256, 148);
+  maps_ratio_kernel<<<g, 256, 0, s>>>(old_infl, new_infl, moves, k, state);
+  maps_global_kernel<<<1, 1, 0, s>>>(k, state, lb_par, flags, reset, scale_hint);
+  maps_cluster_kernel<<<g, 256, 0, s>>>(new_infl, k, state, inv2_lo, inv2_hi, (float4*)ub_eval,
+                                        (float4*)ub_norm, flags, reset, scale_hint);
   return check_launch("update_maps");
 }
 
-int gp_region_maps(const double* old_infl, const double* new_infl, const double* moves, int k,
-                   const int32_t* group_list, const int32_t* group_count, int group_cap,
-                   int64_t nregions, double* rstate, float* rpar, int32_t* flags, int reset,
-                   double scale_hint, void* stream) {
+int gp_region_maps(const double* map_state, int k, const int32_t* group_list,
+                   const int32_t* group_count, int group_cap, int64_t nregions, double* rstate,
+                   float* rpar, int32_t* flags, int reset, double scale_hint, void* stream) {
   GP_REQUIRE(k >= 1 && rstate && rpar && flags && nregions >= 1, "gp_region_maps: bad args");
-  GP_REQUIRE(reset || (old_infl && new_infl && group_list && group_count),
+  GP_REQUIRE(reset || (map_state && group_list && group_count),
              "gp_region_maps: inputs missing");
+  const double* ratio = map_state ? map_state + 2 * k + 6 : nullptr;
   region_maps_kernel<<<grid_for(nregions * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      old_infl, new_infl, moves, k, group_list, group_count, group_cap, nregions, rstate,
+      ratio, ratio ? ratio + k : nullptr, k, group_list, group_count, group_cap, nregions, rstate,
       (float4*)rpar, flags, reset, scale_hint);
   return check_launch("region_maps");
 }

@@ -342,7 +342,7 @@ class DevicePartitioner:
         # influences (ping-pong) | inv2_lo | inv2_hi | moves   (float64)
         self.kstate = torch.empty(5 * k, dtype=torch.float64, device=dev)
         # device bound maps S[k] | T[k] | A | B | steps, and their float32 parameters
-        self.mapstate = torch.empty(2 * k + 3, dtype=torch.float64, device=dev)
+        self.mapstate = torch.empty(4 * k + 6, dtype=torch.float64, device=dev)
         self.kmaps = torch.empty(8 * k + 4, dtype=torch.float32, device=dev)
         self.mapflag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.red = torch.zeros(k + 3, dtype=torch.int64, device=dev)      # block_w | counters
@@ -435,7 +435,7 @@ class DevicePartitioner:
         if not reset:
             h.refresh()                # the lists under the new centers and influences
             self.lists_fresh = True
-        N.call("gp_region_maps", old_ptr, new_ptr, moves_ptr, self.settings.k,
+        N.call("gp_region_maps", self.mapstate.data_ptr(), self.settings.k,
                h.slist.data_ptr(), h.scount.data_ptr(), h.SUPER_CAP, self.rmaps,
                self.rstate.data_ptr(), self.rpar.data_ptr(), self.mapflag.data_ptr(),
                1 if reset else 0, self.scale_hint, self.sh)
@@ -527,7 +527,7 @@ class DevicePartitioner:
         a = self.aargs
         N.call("gp_lb_remap", C.byref(a), 0, self.sh)
         self._alloc_region_maps(self.hier.ns)
-        N.call("gp_region_maps", None, None, None, self.settings.k, None, None, 0, self.rmaps,
+        N.call("gp_region_maps", None, self.settings.k, None, None, 0, self.rmaps,
                self.rstate.data_ptr(), self.rpar.data_ptr(), self.mapflag.data_ptr(), 1,
                self.scale_hint, self.sh)
         a.lb_rpar, a.lb_rshift = self.rpar.data_ptr(), self.hier.SUPER_SHIFT
