@@ -163,8 +163,8 @@ class _Hierarchy:
     start from their super group's list instead of all k centers.
     """
 
-    SUPER_SHIFT, MEGA_SHIFT = 14, 20
-    SUPER_CAP, MEGA_CAP = 1024, 4096
+    SUPER_SHIFT, MEGA_SHIFT, GIGA_SHIFT = 14, 20, 24
+    SUPER_CAP, MEGA_CAP, GIGA_CAP = 1024, 4096, 8192
 
     def __init__(self, eng, use_mega: bool):
         self.eng = weakref.proxy(eng)  # no engine <-> hierarchy cycle keeping GBs alive
@@ -194,6 +194,24 @@ class _Hierarchy:
             self.mcount = torch.empty(self.nm, dtype=torch.int32, device=dev)
             N.call("gp_group_boxes", eng.aargs.X, eng.ldx, d, list_ptr, m,
                    self.MEGA_SHIFT, self.mbox.data_ptr(), eng.sh)
+        # a third level (2^24 entries) when there are many mega groups: the mega
+        # lists then start from a giga list instead of all k
+        self.use_giga = self.use_mega and m > (1 << (self.GIGA_SHIFT + 1))
+        if self.use_giga:
+            self.ng = (m + (1 << self.GIGA_SHIFT) - 1) >> self.GIGA_SHIFT
+            self.glist = torch.empty(self.ng * self.GIGA_CAP, dtype=torch.int32, device=dev)
+            self.gcount = torch.empty(self.ng, dtype=torch.int32, device=dev)
+            # giga boxes = unions of their 16 mega boxes (empty boxes are +inf/-inf)
+            r = 1 << (self.GIGA_SHIFT - self.MEGA_SHIFT)
+            mb = self.mbox.view(self.nm, 2, d)
+            pad = self.ng * r - self.nm
+            if pad:
+                fill = torch.empty((pad, 2, d), dtype=torch.float64, device=dev)
+                fill[:, 0], fill[:, 1] = math.inf, -math.inf
+                mb = torch.cat([mb, fill])
+            mb = mb.view(self.ng, r, 2, d)
+            self.gbox = torch.stack([mb[:, :, 0].amin(dim=1), mb[:, :, 1].amax(dim=1)],
+                                    dim=1).contiguous().view(-1)
         a = eng.aargs
         a.group_list, a.group_count = self.slist.data_ptr(), self.scount.data_ptr()
         a.group_cap, a.group_shift = self.SUPER_CAP, self.SUPER_SHIFT
@@ -205,10 +223,15 @@ class _Hierarchy:
         cen = eng.centers_d.data_ptr()
         i2lo, i2hi = eng.aargs.inv2_lo, eng.aargs.inv2_hi
         parent, pcount, pcap = None, None, 0
+        if self.use_giga:
+            N.call("gp_group_candidates", self.gbox.data_ptr(), self.ng, d, k, cen, i2lo, i2hi,
+                   None, None, 0, 0, self.glist.data_ptr(), self.gcount.data_ptr(),
+                   self.GIGA_CAP, eng.sh)
+            parent, pcount, pcap = self.glist.data_ptr(), self.gcount.data_ptr(), self.GIGA_CAP
         if self.use_mega:
             N.call("gp_group_candidates", self.mbox.data_ptr(), self.nm, d, k, cen, i2lo, i2hi,
-                   None, None, 0, 0, self.mlist.data_ptr(), self.mcount.data_ptr(),
-                   self.MEGA_CAP, eng.sh)
+                   parent, pcount, pcap, self.GIGA_SHIFT - self.MEGA_SHIFT if parent else 0,
+                   self.mlist.data_ptr(), self.mcount.data_ptr(), self.MEGA_CAP, eng.sh)
             parent, pcount, pcap = self.mlist.data_ptr(), self.mcount.data_ptr(), self.MEGA_CAP
         N.call("gp_group_candidates", self.sbox.data_ptr(), self.ns, d, k, cen, i2lo, i2hi,
                parent, pcount, pcap, self.MEGA_SHIFT - self.SUPER_SHIFT,
