@@ -334,3 +334,25 @@ def test_large_k_mega_level_exact_argmin():
     part, stats = balanced_kmeans_points(pts, None, s, return_stats=True)
     st = stats.final_state
     assert np.array_equal(part.assignment, O.brute_labels(pts, st.centers, st.influence))
+
+
+def test_giga_level_exact_argmin(monkeypatch):
+    """The 2^24-entry hierarchy level (active sets above 2^25 entries at the
+    default shifts), exercised at test size with smaller group shifts: results
+    equal the run without it, and the final assignment is the exact argmin."""
+    from paper_1805_01208_b200.kmeans import _Hierarchy
+
+    O = _oracle()
+    rng = np.random.default_rng(23)
+    pts = rng.random((240_000, 2))
+    pts[:60_000] = 0.3 + 0.04 * rng.standard_normal((60_000, 2))
+    s = KMeansSettings(k=4500, seed=0, max_iter=3, max_balance_iter=4)
+    base = balanced_kmeans_points(pts, None, s, return_stats=True)
+    monkeypatch.setattr(_Hierarchy, "MEGA_SHIFT", 13)
+    monkeypatch.setattr(_Hierarchy, "GIGA_SHIFT", 15)
+    monkeypatch.setenv("GP_SUPER_SHIFT", "10")
+    part, stats = balanced_kmeans_points(pts, None, s, return_stats=True)
+    st = stats.final_state
+    assert np.array_equal(part.assignment, base[0].assignment)
+    assert np.array_equal(st.centers, base[1].final_state.centers)
+    assert np.array_equal(part.assignment, O.brute_labels(pts, st.centers, st.influence))
