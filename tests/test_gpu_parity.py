@@ -356,3 +356,23 @@ def test_giga_level_exact_argmin(monkeypatch):
     assert np.array_equal(part.assignment, base[0].assignment)
     assert np.array_equal(st.centers, base[1].final_state.centers)
     assert np.array_equal(part.assignment, O.brute_labels(pts, st.centers, st.influence))
+
+
+@pytest.mark.parametrize("scale,offset", [(1e-9, 0.0), (1e9, 0.0), (1.0, 1e6), (1.0, 0.0)])
+def test_fp16_bound_storage_extreme_scales(scale, offset):
+    """Bounds are stored as fp16 pairs times a power-of-two scale: tiny,
+    huge and offset coordinate ranges, and a cluster 1e-6 the size of the box, keep
+    results identical to the oracle (storage precision only moves skip decisions)."""
+    O = _oracle()
+    rng = np.random.default_rng(31)
+    pts = rng.random((30_000, 2))
+    if scale == 1.0 and offset == 0.0:
+        pts[:10_000] = 0.25 + 1e-6 * rng.random((10_000, 2))   # mixed scales
+    pts = pts * scale + offset
+    s = KMeansSettings(k=24, seed=0, max_iter=8)
+    part, stats = balanced_kmeans_points(pts, None, s, return_stats=True)
+    r = O.run(pts, None, O.Knobs(k=24, seed=0, max_iter=8))
+    assert np.array_equal(part.assignment, r.assignment)
+    assert np.array_equal(stats.final_state.centers, r.centers)
+    assert np.array_equal(stats.final_state.influence, r.influence)
+    _compare_records(stats.iterations, r.records)
