@@ -192,6 +192,9 @@ typedef struct gp_assign_args {
   /* power of two applied to the stored fp16 bounds (keeps them in fp16's normal range;
    * about 1 / the box diagonal) */
   float bound_scale;
+  /* device copy of inv2_min kept by gp_update_maps (map_state + 2k + 7); when set it
+   * replaces inv2_min, so a captured loop graph sees every round's value */
+  const double* inv2_min_dev;
 } gp_assign_args;
 int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);
@@ -218,9 +221,11 @@ int gp_group_candidates(const double* boxes, int64_t ngroups, int d, int k,
 
 /* Device-side bound-map bookkeeping (control.BoundMaps on the GPU): compose one
  * relaxation (kmeans.py:208-239) old_infl -> new_infl with center moves `moves`
- * (NULL = zero moves) into the cumulative maps `state` (4k + 6 doubles: S[k], T[k],
- * A, B, steps, 3 scratch, then this relaxation's per-cluster ratio I_old/I_new [k]
- * and shift move/I_new [k]), unless it is the reference's identity early return, and
+ * (NULL = zero moves) into the cumulative maps `state` (4k + 8 doubles: S[k], T[k],
+ * A, B, steps, 5 scratch (min ratio, max shift, changed, max influence, inv2_min =
+ * 1 / max(infl)^2 * (1 - 1e-15)), then this relaxation's per-cluster ratio
+ * I_old/I_new [k] and shift move/I_new [k]), unless it is the reference's identity
+ * early return, and
  * derive every parameter the kernels read: inv2_lo/inv2_hi (k), ub_eval/ub_norm
  * (k x 4 floats), lb_par (4 floats).  flags[0] is set to 1 when the maps should
  * be re-based (gp_rebase_bounds + gp_reset_maps).  reset != 0 starts from
@@ -331,6 +336,36 @@ int gp_scatter_by_gid(const int32_t* a, const uint32_t* gids, int64_t n, int64_t
  * (kmeans.py:568). */
 int gp_gather_ranks(const int32_t* rank_by_gid, const uint32_t* gids, int64_t n, int32_t* out,
                     void* stream);
+
+/* ---- device-resident loops ------------------------------------------------ */
+/* A CUDA graph with one conditional WHILE node whose body is captured from the
+ * work issued on `stream` between gp_loop_graph_begin and gp_loop_graph_end
+ * (stream capture into the body graph).  A body kernel decides whether the loop
+ * runs again (cudaGraphSetConditional on gp_loop_graph_handle(ctx)).  Used for
+ * the balance rounds of one movement iteration (kmeans.py:415-443): the host
+ * launches the whole loop and synchronises once.  gp_loop_test_countdown is a
+ * body kernel for tests: --*counter, loop while it is positive. */
+int gp_loop_graph_begin(void* stream, void** ctx);
+unsigned long long gp_loop_graph_handle(void* ctx);
+int gp_loop_graph_end(void* ctx);
+int gp_loop_graph_launch(void* ctx, void* stream);
+int gp_loop_graph_destroy(void* ctx);
+int gp_loop_test_countdown(int* counter, unsigned long long handle, void* stream);
+
+/* One balance-round decision of assign_and_balance (kmeans.py:425-443) on the
+ * device, for the loop graph (d = 2, exact block weights): from the round's
+ * block-weight units and counters red[k + 3] (gp_assign_round), the block
+ * weights units / wscale, imbalance (metrics.py:33-40), the stop test
+ * (imbalance <= eps or the last round), the step halving from the second
+ * regression, and, when the loop goes on, next[c] = cur[c] * clip(sqrt(target /
+ * w_c), 1 - cap, 1 + cap) (kmeans.py:176-191 with d = 2: numpy's x ** 0.5 is
+ * sqrt).  bal (doubles): [0] cap, [1] regressions, [2] best imbalance, [3] rounds
+ * done, [4] error (target <= 0 or total <= 0), [5..7] unused, then the per-round
+ * imbalance, skips and distance evaluations (max_rounds each).  handle != 0:
+ * sets the loop graph's condition to "run again". */
+int gp_balance_decide(const long long* red, int k, double wscale, double eps, int max_rounds,
+                      double* bal, const double* infl_cur, double* infl_next,
+                      unsigned long long handle, void* stream);
 
 /* ---- callers of the path ---------------------------------- */
 

@@ -34,7 +34,7 @@ class AssignArgs(C.Structure):
         ("workspace", vp), ("workspace_bytes", sz), ("scan_regions", i32), ("grid_n", i32),
         ("grid_start", vp), ("grid_items", vp), ("grid_lo", f64 * 3), ("grid_h", f64),
         ("inv2_min", f64), ("unit_boxes", vp), ("unit_shift", i32), ("flags", i32),
-        ("lb_rpar", vp), ("lb_rshift", i32), ("bound_scale", C.c_float),
+        ("lb_rpar", vp), ("lb_rshift", i32), ("bound_scale", C.c_float), ("inv2_min_dev", vp),
     ]
 
 
@@ -89,6 +89,13 @@ _SIGS = {
                                   vp]),
     "gp_scatter_state": (C.c_int, [vp, i64, vp, vp, vp, vp, vp]),
     "gp_gather_ranks": (C.c_int, [vp, vp, i64, vp, vp]),
+    "gp_loop_graph_begin": (C.c_int, [vp, C.POINTER(vp)]),
+    "gp_loop_graph_handle": (u64, [vp]),
+    "gp_loop_graph_end": (C.c_int, [vp]),
+    "gp_loop_graph_launch": (C.c_int, [vp, vp]),
+    "gp_loop_graph_destroy": (C.c_int, [vp]),
+    "gp_loop_test_countdown": (C.c_int, [vp, u64, vp]),
+    "gp_balance_decide": (C.c_int, [vp, C.c_int, f64, f64, C.c_int, vp, vp, vp, u64, vp]),
     "gp_sfc_cut_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_sfc_cut": (C.c_int, [vp, vp, i64, C.c_int, f64, vp, vp, sz, vp]),
     "gp_predict": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]),
@@ -131,7 +138,7 @@ KERNELS_PER_CALL = {
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
     "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 3, "gp_region_maps": 1, "gp_lb_remap": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
-    "gp_sfc_cut": 3, "gp_predict": 1,
+    "gp_sfc_cut": 3, "gp_predict": 1, "gp_balance_decide": 1,
 }
 _launches = [0]
 calls: dict[str, int] = {}   # API calls by name (tools/kprof.py)

@@ -67,6 +67,12 @@ __device__ __forceinline__ void store_bounds(const gp_assign_args& p, const floa
       bnd_pack(ub_normf(N, b_up), lb_normf(L.z, L.w, s_dn), p.bound_scale);
 }
 
+// lower bound of min_c 1/infl_c^2: the device copy gp_update_maps keeps (so that a
+// captured loop graph sees every round's value), else the host scalar
+__device__ __forceinline__ double inv2_min_of(const gp_assign_args& p) {
+  return p.inv2_min_dev ? *p.inv2_min_dev : p.inv2_min;
+}
+
 // lower-bound map parameters (A_lo, B_hi, 1/A_lo, B_lo) of active entry li: its
 // region's (gp_region_maps) or the global ones
 __device__ __forceinline__ float4 lb_params(const gp_assign_args& p, int64_t li) {
@@ -525,7 +531,7 @@ __device__ void grid_point(const gp_assign_args& p, const double* x, int& bi, fl
     for (int j = 0; j < D; ++j) covered = covered && cc[j] - r <= 0 && cc[j] + r >= G - 1;
     if (covered) break;
     const double rh = (double)r * p.grid_h;
-    const double bound = __dmul_rd(__dmul_rd(rh, rh), p.inv2_min) * (1.0 - 1e-9);
+    const double bound = __dmul_rd(__dmul_rd(rh, rh), inv2_min_of(p)) * (1.0 - 1e-9);
     if (bound > fma(q2, Q_TOL, q2)) break;
   }
   const double thr = fma(q2, Q_TOL, q2);
@@ -667,7 +673,7 @@ __global__ void __launch_bounds__(WKT) walk_kernel(gp_assign_args p, int wshift,
       for (int j = 0; j < D; ++j) covered = covered && cc[j] - rr <= 0 && cc[j] + rr >= G - 1;
       if (covered) break;
       const double rh = (double)rr * p.grid_h;
-      const double bound = __dmul_rd(__dmul_rd(rh, rh), p.inv2_min) * (1.0 - 1e-9);
+      const double bound = __dmul_rd(__dmul_rd(rh, rh), inv2_min_of(p)) * (1.0 - 1e-9);
       if (bound > fma(m2, Q_TOL, m2)) break;
     }
     // union of the lanes' top-3 lists (every center was evaluated by one lane)
@@ -1264,19 +1270,21 @@ constexpr double UBS = 1.0 + 1e-12, LBS = 1.0 - 1e-12;
 //     changed" as order-preserving atomics (both are >= 0);
 //  2. maps_global_kernel (one thread): the lower-bound map A, B, steps and lb_par;
 //  3. maps_cluster_kernel: the per-cluster maps and parameters.
-// state layout: S[k] | T[k] | A, B, steps | rmin, smax, any (scratch) | ratio[k] | shift[k]
+// state layout: S[k] | T[k] | A, B, steps | rmin, smax, any, max infl, inv2_min |
+//               ratio[k] | shift[k]   (gp_map_state_size)
 __global__ void maps_ratio_kernel(const double* __restrict__ old_infl,
                                   const double* __restrict__ new_infl,
                                   const double* __restrict__ moves, int k,
                                   double* __restrict__ st) {
   double* scr = st + 2 * k + 3;
-  double* ratio = st + 2 * k + 6;
+  double* ratio = st + 2 * k + 8;
   double* shift = ratio + k;
-  double rmin = INFINITY, smax = 0.0;
+  double rmin = INFINITY, smax = 0.0, imax = 0.0;
   int any = 0;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
     const double mv = moves ? moves[c] : 0.0;
     any |= (mv != 0.0) || (old_infl[c] != new_infl[c]);
+    imax = fmax(imax, new_infl[c]);
     const double r = old_infl[c] / new_infl[c];
     const double sh = mv / new_infl[c];
     ratio[c] = r;
@@ -1287,6 +1295,7 @@ __global__ void maps_ratio_kernel(const double* __restrict__ old_infl,
   for (int o = 16; o; o >>= 1) {
     rmin = fmin(rmin, __shfl_xor_sync(FULL, rmin, o));
     smax = fmax(smax, __shfl_xor_sync(FULL, smax, o));
+    imax = fmax(imax, __shfl_xor_sync(FULL, imax, o));
     any |= __shfl_xor_sync(FULL, any, o);
   }
   if ((threadIdx.x & 31) == 0) {
@@ -1294,6 +1303,7 @@ __global__ void maps_ratio_kernel(const double* __restrict__ old_infl,
     atomicMin(&u[0], (unsigned long long)__double_as_longlong(rmin));   // doubles >= 0
     atomicMax(&u[1], (unsigned long long)__double_as_longlong(smax));
     if (any) atomicOr(&u[2], 1ull);
+    atomicMax(&u[3], (unsigned long long)__double_as_longlong(imax));
   }
 }
 
@@ -1303,6 +1313,9 @@ __global__ void maps_global_kernel(int k, double* __restrict__ st, float* __rest
   const unsigned long long* u = reinterpret_cast<const unsigned long long*>(st + 2 * k + 3);
   const double rmin = __longlong_as_double((long long)u[0]);
   const double smax = __longlong_as_double((long long)u[1]);
+  // the host's 1.0 / float(max(infl)) ** 2 * (1.0 - 1e-15), on the device
+  const double imax = __longlong_as_double((long long)u[3]);
+  st[2 * k + 7] = __dmul_rn(__ddiv_rn(1.0, __dmul_rn(imax, imax)), 1.0 - 1e-15);
   // relax_bounds' identity early return (kmeans.py:223-228)
   const bool compose = !reset && u[2] != 0;
   double A = reset ? 1.0 : ABs[0], B = reset ? 0.0 : ABs[1], steps = reset ? 0.0 : ABs[2];
@@ -1332,7 +1345,7 @@ __global__ void maps_cluster_kernel(const double* __restrict__ new_infl, int k,
   const double steps = st[2 * k + 2];   // already composed by maps_global_kernel
   const unsigned long long any = reinterpret_cast<const unsigned long long*>(st + 2 * k + 3)[2];
   const bool compose = !reset && any != 0;
-  const double* ratio = st + 2 * k + 6;
+  const double* ratio = st + 2 * k + 8;
   const double* shift = ratio + k;
   const double e = (4.0 * steps + 16.0) * 0x1p-52;
   int out_of_range = 0;
@@ -1362,15 +1375,19 @@ __global__ void maps_cluster_kernel(const double* __restrict__ new_infl, int k,
 // list (all k when the list overflowed), composed into its lower-bound map like
 // update_maps_kernel composes the global one
 __global__ void __launch_bounds__(256) region_maps_kernel(
-    const double* __restrict__ ratio, const double* __restrict__ shift, int k,
-    const int32_t* __restrict__ glist,
+    const double* __restrict__ ratio, const double* __restrict__ shift,
+    const unsigned long long* __restrict__ any, int k, const int32_t* __restrict__ glist,
     const int32_t* __restrict__ gcount, int gcap, int64_t R, double* __restrict__ rst,
     float4* __restrict__ rpar, int32_t* __restrict__ flags, int reset, double scale_hint) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (r >= R) return;
   double A = 1.0, B = 0.0, steps = 0.0;
-  if (!reset) {
+  if (!reset && any && *any == 0) {   // identity relaxation: keep the map
+    A = rst[3 * r];
+    B = rst[3 * r + 1];
+    steps = rst[3 * r + 2];
+  } else if (!reset) {
     const int gc = gcount[r];
     const int32_t* lst = gc >= 0 ? glist + r * (int64_t)gcap : nullptr;
     const int ns = gc >= 0 ? gc : k;
@@ -1539,7 +1556,7 @@ int gp_update_maps(const double* old_infl, const double* new_infl, const double*
   cudaStream_t s = (cudaStream_t)stream;
   double* scr = state + 2 * k + 3;
   GP_CUDA(cudaMemsetAsync(scr, 0xff, sizeof(double), s));            // rmin: +max key
-  GP_CUDA(cudaMemsetAsync(scr + 1, 0, 2 * sizeof(double), s));       // smax, any
+  GP_CUDA(cudaMemsetAsync(scr + 1, 0, 3 * sizeof(double), s));       // smax, any, max infl
   const unsigned g = grid_for(k, 256, 148);
   maps_ratio_kernel<<<g, 256, 0, s>>>(old_infl, new_infl, moves, k, state);
   maps_global_kernel<<<1, 1, 0, s>>>(k, state, lb_par, flags, reset, scale_hint);
@@ -1554,10 +1571,13 @@ int gp_region_maps(const double* map_state, int k, const int32_t* group_list,
   GP_REQUIRE(k >= 1 && rstate && rpar && flags && nregions >= 1, "gp_region_maps: bad args");
   GP_REQUIRE(reset || (map_state && group_list && group_count),
              "gp_region_maps: inputs missing");
-  const double* ratio = map_state ? map_state + 2 * k + 6 : nullptr;
+  const double* ratio = map_state ? map_state + 2 * k + 8 : nullptr;
+  // the reference's identity early return (nothing moved or changed) holds here too
+  const unsigned long long* any =
+      map_state ? reinterpret_cast<const unsigned long long*>(map_state + 2 * k + 5) : nullptr;
   region_maps_kernel<<<grid_for(nregions * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      ratio, ratio ? ratio + k : nullptr, k, group_list, group_count, group_cap, nregions, rstate,
-      (float4*)rpar, flags, reset, scale_hint);
+      ratio, ratio ? ratio + k : nullptr, any, k, group_list, group_count, group_cap, nregions,
+      rstate, (float4*)rpar, flags, reset, scale_hint);
   return check_launch("region_maps");
 }
 

@@ -365,7 +365,7 @@ class DevicePartitioner:
         # influences (ping-pong) | inv2_lo | inv2_hi | moves   (float64)
         self.kstate = torch.empty(5 * k, dtype=torch.float64, device=dev)
         # device bound maps S[k] | T[k] | A | B | steps, and their float32 parameters
-        self.mapstate = torch.empty(4 * k + 6, dtype=torch.float64, device=dev)
+        self.mapstate = torch.empty(4 * k + 8, dtype=torch.float64, device=dev)
         self.kmaps = torch.empty(8 * k + 4, dtype=torch.float32, device=dev)
         self.mapflag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.red = torch.zeros(k + 3, dtype=torch.int64, device=dev)      # block_w | counters
@@ -392,6 +392,7 @@ class DevicePartitioner:
         a.infl, a.inv2_lo, a.inv2_hi = base, base + 16 * k, base + 24 * k
         mb = self.kmaps.data_ptr()
         a.ub_eval, a.ub_norm, a.lb_par = mb, mb + 16 * k, mb + 32 * k
+        a.inv2_min_dev = self.mapstate.data_ptr() + 8 * (2 * k + 7)   # kept by gp_update_maps
         a.block_w = self.red.data_ptr()
         a.counters = self.red.data_ptr() + 8 * k
         awb = N.size_query("gp_assign_workspace_bytes", n)
@@ -710,40 +711,11 @@ class DevicePartitioner:
             if phase == "full" and self.hier is not None and self.rmaps is None:
                 self._enter_region_maps(infl)
             # ---------------- assign_and_balance (kmeans.py:377-453)
-            skips = decisions = evals = 0
-            final_imb = math.inf
-            best_imb = math.inf
-            cap = st.influence_step_cap
-            regressions = 0
-            history = []
-            rounds = 0
-            for rnd in range(st.max_balance_iter):
-                rounds += 1
-                if st.audit_bounds:
-                    N.count("gp_audit")
-                    N.check(N.lib.gp_audit(C.byref(self.aargs), self.audit_out.data_ptr(), self.sh),
-                            "gp_audit")
-                blk, cnt = self._assign()
-                skips += int(cnt[0])
-                decisions += int(cnt[1])
-                evals += int(cnt[2])
-                block_w = self._block_weights(blk)
-                final_imb = imbalance(block_w)
-                history.append(final_imb)
-                if final_imb <= st.epsilon or rnd == st.max_balance_iter - 1:
-                    break
-                if final_imb > best_imb:
-                    regressions += 1
-                    if regressions >= 2:
-                        cap *= 0.5
-                best_imb = min(best_imb, final_imb)
-                target = float(block_w.sum()) / k
-                if not target > 0:
-                    raise ValueError("target weight must be positive")
-                new_infl = infl * influence_factor(block_w, target, cap, d)
-                infl = new_infl
-                self._set_influence(infl)
-            info = BalanceInfo(rounds, final_imb, block_w, skips, decisions, evals, history)
+            if self._graph_ok():
+                info, infl = self._balance_graph(infl)
+            else:
+                info, infl = self._balance_host(infl)
+            block_w = info.block_weights
             self._leave_dense()
             if phase == "full" and info.imbalance <= st.epsilon:
                 # the assignment at this point is the exact argmin under (centers, infl);
@@ -814,6 +786,167 @@ class DevicePartitioner:
         self.release()
         return out, stats
 
+    # ------------------------------------------------------------ loop graphs
+    def _graph_ok(self) -> bool:
+        """The balance rounds can run as one device-resident loop graph when every
+        decision of the round is reproducible on the device: d = 2 (the influence
+        step is a sqrt), exact integer block weights, one GPU, no audit or
+        per-round statistics.  Opt-in (GP_BALANCE_GRAPH=full|all): measured slower
+        than the host-driven rounds this round."""
+        mode = os.environ.get("GP_BALANCE_GRAPH", "0")
+        if mode == "0" or not (type(self) is DevicePartitioner and self.d == 2
+                               and self.wplan.exact and not self.settings.audit_bounds
+                               and not (self.aargs.flags & 1)):
+            return False
+        # a warm-up sample step has a new active set (a new capture) and ~20 short
+        # rounds: capturing there costs more than it saves, so by default only the
+        # full phase, whose iterations all share one graph, uses it ("all": every phase)
+        return mode == "all" or (self.aargs.list is None and not getattr(self, "dense_m", 0))
+
+    def _balance_graph(self, infl):
+        """assign_and_balance (kmeans.py:377-453) as a CUDA graph with a conditional
+        WHILE node: each pass applies the previous pass's influence step (bound maps,
+        candidate lists, region maps; the identity on the first pass), runs the
+        assign round and decides on the device (gp_balance_decide) whether to go on.
+        The host launches the loop once and reads the per-round records after it."""
+        st, k, a = self.settings, self.settings.k, self.aargs
+        mr = st.max_balance_iter
+        if getattr(self, "bal", None) is None or self.bal.numel() < 8 + 3 * mr:
+            self.bal = torch.empty(8 + 3 * mr, dtype=torch.float64, device=self.device)
+            self.bal_h = torch.empty(8 + 3 * mr, dtype=torch.float64, pin_memory=True)
+            self.bal_init = torch.empty(8, dtype=torch.float64, pin_memory=True)
+            self.loop_graphs = {}
+        cur, nxt = self.cur, 1 - self.cur
+        cur_p, nxt_p = self._infl_ptr(cur), self._infl_ptr(nxt)
+        key = (cur, a.X, a.a, a.ublb, a.list, a.m, a.flags, a.scan_regions, a.unit_boxes,
+               a.unit_shift, a.lb_rpar, a.group_list, a.group_count, a.grid_start, a.grid_n,
+               self.rmaps, self.walk, getattr(self.hier, "key", None), mr, st.epsilon,
+               self.wplan.scale, a.workspace)
+        ctx = self.loop_graphs.get(key)
+        if ctx is None:
+            for old in self.loop_graphs.values():
+                N.lib.gp_loop_graph_destroy(old)
+            self.loop_graphs = {}
+            # capture on a side stream (the legacy default stream cannot capture);
+            # the graph itself is launched on the partition's stream
+            if getattr(self, "cap_stream", None) is None:
+                self.cap_stream = torch.cuda.Stream(self.device)
+            self.cap_stream.wait_stream(self.stream)
+            sh = self.sh
+            self.sh = self.cap_stream.cuda_stream
+            try:
+                with torch.cuda.stream(self.cap_stream):
+                    ctx = self._capture_balance_graph(cur_p, nxt_p)
+            finally:
+                self.sh = sh
+            self.loop_graphs[key] = ctx
+        # loop state: cap, regressions, best imbalance, rounds, error; next := cur so
+        # the first pass's influence step is the identity
+        self.bal_init.numpy()[:] = [st.influence_step_cap, 0.0, math.inf, 0.0, 0.0, 0.0, 0.0, 0.0]
+        self.bal[:8].copy_(self.bal_init, non_blocking=True)
+        self.kstate[nxt * k:(nxt + 1) * k].copy_(self.kstate[cur * k:(cur + 1) * k])
+        if self.timer is not None:
+            e0 = self.timer.mark(self.stream)
+        N.count("gp_assign_round")
+        N.check(N.lib.gp_loop_graph_launch(ctx, self.sh), "gp_loop_graph_launch")
+        if self.timer is not None:
+            self.timer.events.append((e0, self.timer.mark(self.stream)))
+        self.red_h.copy_(self.red, non_blocking=True)
+        self.bal_h.copy_(self.bal, non_blocking=True)
+        self.stream.synchronize()
+        bal = self.bal_h.numpy()
+        rounds = int(bal[3])
+        N._launches[0] += rounds * self.graph_kernels
+        if bal[4] != 0.0:
+            raise ValueError("target weight must be positive")
+        hist = [float(v) for v in bal[8:8 + rounds]]
+        skips_r = bal[8 + mr:8 + mr + rounds].astype(np.int64)
+        evals_r = bal[8 + 2 * mr:8 + 2 * mr + rounds].astype(np.int64)
+        blk = self.red_h.numpy()[:k].copy()
+        block_w = self._block_weights(blk)
+        if rounds > 1:   # the influences the last round used
+            infl = self.kstate[cur * k:(cur + 1) * k].cpu().numpy().copy()
+            a.inv2_min = 1.0 / float(np.max(infl)) ** 2 * (1.0 - 1e-15)
+        if self.timer is not None:
+            for sk, ev in zip(skips_r, evals_r):
+                self.timer.rounds.append((self.m_global, int(self.m_global - sk), int(ev)))
+        self.lists_fresh = False
+        info = BalanceInfo(rounds, hist[-1], block_w, int(skips_r.sum()),
+                           rounds * self.m_global, int(evals_r.sum()), hist)
+        return info, infl
+
+    def _capture_balance_graph(self, cur_p, nxt_p):
+        k, a, sh = self.settings.k, self.aargs, self.sh
+        ctx = C.c_void_p()
+        c0 = N.launch_count()
+        N.check(N.lib.gp_loop_graph_begin(sh, C.byref(ctx)), "gp_loop_graph_begin")
+        try:
+            handle = N.lib.gp_loop_graph_handle(ctx)
+            # the previous pass's influence step (kmeans.py:437-443): maps cur -> next,
+            # candidate lists and region maps under the new influences, then next -> cur
+            mb = self.kmaps.data_ptr()
+            N.call("gp_update_maps", cur_p, nxt_p, None, k, self.mapstate.data_ptr(),
+                   a.inv2_lo, a.inv2_hi, mb, mb + 16 * k, mb + 32 * k, self.mapflag.data_ptr(),
+                   0, self.scale_hint, sh)
+            if self.rmaps is not None:
+                self._relax_regions(cur_p, nxt_p, None, False)
+            elif self.hier is not None and not self.walk:
+                self.hier.refresh()
+            cur_t = self.kstate[self.cur * k:(self.cur + 1) * k]
+            nxt_t = self.kstate[(1 - self.cur) * k:(2 - self.cur) * k]
+            cur_t.copy_(nxt_t)
+            # the round (kmeans.py:415-425) and its decision (kmeans.py:426-443)
+            self.red.zero_()
+            N.check(N.lib.gp_assign_round(C.byref(a), sh), "gp_assign_round")
+            N.call("gp_balance_decide", self.red.data_ptr(), k, float(self.wplan.scale),
+                   float(self.settings.epsilon), self.settings.max_balance_iter,
+                   self.bal.data_ptr(), cur_p, nxt_p, handle, sh)
+        finally:
+            N.check(N.lib.gp_loop_graph_end(ctx), "gp_loop_graph_end")
+        # kernels per pass (the captured calls did not launch anything yet)
+        self.graph_kernels = N.launch_count() - c0 + 3   # + zero_, copy, assign round
+        N._launches[0] = c0
+        return ctx
+
+    def _balance_host(self, infl):
+        """assign_and_balance (kmeans.py:377-453) with one host round trip per round."""
+        st, d, k = self.settings, self.d, self.settings.k
+        skips = decisions = evals = 0
+        final_imb = math.inf
+        best_imb = math.inf
+        cap = st.influence_step_cap
+        regressions = 0
+        history = []
+        rounds = 0
+        for rnd in range(st.max_balance_iter):
+            rounds += 1
+            if st.audit_bounds:
+                N.count("gp_audit")
+                N.check(N.lib.gp_audit(C.byref(self.aargs), self.audit_out.data_ptr(), self.sh),
+                        "gp_audit")
+            blk, cnt = self._assign()
+            skips += int(cnt[0])
+            decisions += int(cnt[1])
+            evals += int(cnt[2])
+            block_w = self._block_weights(blk)
+            final_imb = imbalance(block_w)
+            history.append(final_imb)
+            if final_imb <= st.epsilon or rnd == st.max_balance_iter - 1:
+                break
+            if final_imb > best_imb:
+                regressions += 1
+                if regressions >= 2:
+                    cap *= 0.5
+            best_imb = min(best_imb, final_imb)
+            target = float(block_w.sum()) / k
+            if not target > 0:
+                raise ValueError("target weight must be positive")
+            new_infl = infl * influence_factor(block_w, target, cap, d)
+            infl = new_infl
+            self._set_influence(infl)
+        info = BalanceInfo(rounds, final_imb, block_w, skips, decisions, evals, history)
+        return info, infl
+
     def _recompute(self, state: ClusterState):
         """The fallback assignment (kmeans.py:583-584, 627-630): one assign round from
         cold bounds under the fallback centers and influences reproduces it exactly."""
@@ -835,6 +968,9 @@ class DevicePartitioner:
 
     def release(self):
         """Drop every n-sized device buffer (the caller keeps only the result)."""
+        for ctx in getattr(self, "loop_graphs", {}).values():
+            N.lib.gp_loop_graph_destroy(ctx)
+        self.loop_graphs = {}
         for name in ("X", "W", "A", "UBLB", "A_d", "UBLB_d", "X_d", "W_d", "gids", "rank_sfc", "active_idx",
                      "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier", "grid_start",
                      "grid_items", "ubox", "rstate", "rpar"):

@@ -48,6 +48,7 @@ for r in stats.iterations[::4] + stats.iterations[-3:]:
     print(r.phase, r.active_points, r.balance_rounds, sc // max(r.balance_rounds, 1),
           round(r.distance_evals / max(sc, 1), 2))
 
+os.environ["GP_BALANCE_GRAPH"] = "0"  # per-round timing needs the host-driven rounds
 t = _Timer()
 out, stats = partition_device(pts_d, w_d, s, device=dev, timer=t)
 torch.cuda.synchronize()
