@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(1024) balance_decide_kernel(
       }
     }
     bal[3] = (double)(r + 1);
+    bal[5] = stop ? 1.0 : 0.0;
     s_stop = stop;
     s_tgt = tgt;
     s_cap = cap;

@@ -713,6 +713,8 @@ class DevicePartitioner:
             # ---------------- assign_and_balance (kmeans.py:377-453)
             if self._graph_ok():
                 info, infl = self._balance_graph(infl)
+            elif self._device_decide_ok():
+                info, infl = self._balance_device(infl)
             else:
                 info, infl = self._balance_host(infl)
             block_w = info.block_weights
@@ -907,6 +909,83 @@ class DevicePartitioner:
         self.graph_kernels = N.launch_count() - c0 + 3   # + zero_, copy, assign round
         N._launches[0] = c0
         return ctx
+
+    def _device_decide_ok(self) -> bool:
+        """Same conditions as the loop graph: the round's decision and influence step
+        run on the device (gp_balance_decide) and the host only reads a few scalars
+        per round.  GP_DEVICE_DECIDE=0 turns it off."""
+        return (type(self) is DevicePartitioner and self.d == 2 and self.wplan.exact
+                and not self.settings.audit_bounds and not (self.aargs.flags & 1)
+                and os.environ.get("GP_DEVICE_DECIDE", "1") != "0")
+
+    def _balance_device(self, infl):
+        """assign_and_balance (kmeans.py:377-453) driven by the host, decided on the
+        device: per round the assign kernels, gp_balance_decide (imbalance, stop
+        test, step halving and the next influences), a read-back of its record
+        (6 doubles) and, when the loop goes on, the bound-map / candidate-list /
+        region-map update from the device influences.  No k-sized host math or
+        transfers inside the loop."""
+        st, k, a = self.settings, self.settings.k, self.aargs
+        mr = st.max_balance_iter
+        if getattr(self, "bal", None) is None or self.bal.numel() < 8 + 3 * mr:
+            self.bal = torch.empty(8 + 3 * mr, dtype=torch.float64, device=self.device)
+            self.bal_h = torch.empty(8 + 3 * mr, dtype=torch.float64, pin_memory=True)
+            self.bal_init = torch.empty(8, dtype=torch.float64, pin_memory=True)
+            self.loop_graphs = {}
+        cur, nxt = self.cur, 1 - self.cur
+        cur_p, nxt_p = self._infl_ptr(cur), self._infl_ptr(nxt)
+        cur_t = self.kstate[cur * k:(cur + 1) * k]
+        nxt_t = self.kstate[nxt * k:(nxt + 1) * k]
+        self.bal_init.numpy()[:] = [st.influence_step_cap, 0.0, math.inf, 0.0, 0.0, 0.0, 0.0, 0.0]
+        self.bal[:8].copy_(self.bal_init, non_blocking=True)
+        mb = self.kmaps.data_ptr()
+        bh = self.bal_h.numpy()
+        rounds = 0
+        for rnd in range(mr):
+            if rnd > 0:
+                # the influence step decided last round (kmeans.py:437-443)
+                N.call("gp_update_maps", cur_p, nxt_p, None, k, self.mapstate.data_ptr(),
+                       a.inv2_lo, a.inv2_hi, mb, mb + 16 * k, mb + 32 * k,
+                       self.mapflag.data_ptr(), 0, self.scale_hint, self.sh)
+                if self.rmaps is not None:
+                    self._relax_regions(cur_p, nxt_p, None, False)
+                cur_t.copy_(nxt_t)
+            if self.hier is not None and not self.lists_fresh and not self.walk:
+                self.hier.refresh()
+            self.lists_fresh = False
+            self.red.zero_()
+            if self.timer is not None:
+                e0 = self.timer.mark(self.stream)
+            N.count("gp_assign_round")
+            N.check(N.lib.gp_assign_round(C.byref(a), self.sh), "gp_assign_round")
+            if self.timer is not None:
+                self.timer.events.append((e0, self.timer.mark(self.stream)))
+            N.call("gp_balance_decide", self.red.data_ptr(), k, float(self.wplan.scale),
+                   float(st.epsilon), mr, self.bal.data_ptr(), cur_p, nxt_p, 0, self.sh)
+            self.bal_h[:8].copy_(self.bal[:8], non_blocking=True)
+            self.stream.synchronize()
+            rounds += 1
+            if bh[4] != 0.0:
+                raise ValueError("target weight must be positive")
+            if bh[5] != 0.0:    # stop (the next influences were not written)
+                break
+        self.red_h.copy_(self.red, non_blocking=True)
+        self.bal_h.copy_(self.bal, non_blocking=True)
+        self.stream.synchronize()
+        bal = self.bal_h.numpy()
+        hist = [float(v) for v in bal[8:8 + rounds]]
+        skips_r = bal[8 + mr:8 + mr + rounds].astype(np.int64)
+        evals_r = bal[8 + 2 * mr:8 + 2 * mr + rounds].astype(np.int64)
+        block_w = self._block_weights(self.red_h.numpy()[:k].copy())
+        if rounds > 1:   # the influences the last round used
+            infl = cur_t.cpu().numpy().copy()
+            a.inv2_min = 1.0 / float(np.max(infl)) ** 2 * (1.0 - 1e-15)
+        if self.timer is not None:
+            for sk, ev in zip(skips_r, evals_r):
+                self.timer.rounds.append((self.m_global, int(self.m_global - sk), int(ev)))
+        info = BalanceInfo(rounds, hist[-1], block_w, int(skips_r.sum()),
+                           rounds * self.m_global, int(evals_r.sum()), hist)
+        return info, infl
 
     def _balance_host(self, infl):
         """assign_and_balance (kmeans.py:377-453) with one host round trip per round."""

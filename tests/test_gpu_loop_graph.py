@@ -44,7 +44,8 @@ def test_while_graph_countdown():
 
 @pytest.mark.parametrize("k,weights", [(16, None), (300, "int")])
 def test_balance_graph_modes_bit_identical(monkeypatch, k, weights):
-    """The device-resident balance loop (every phase, full phase only, off) gives
+    """The balance-round drivers (loop graph in every phase or the full phase only,
+    host loop with on-device decisions, host loop with host numpy decisions) give
     the same partition, state and per-iteration records bit for bit, and the
     oracle's."""
     import numpy as np
@@ -57,8 +58,9 @@ def test_balance_graph_modes_bit_identical(monkeypatch, k, weights):
     w = rng.integers(1, 7, 40_000).astype(float) if weights else None
     s = KMeansSettings(k=k, seed=0, max_iter=10)
     runs = {}
-    for mode in ("0", "full", "all"):
-        monkeypatch.setenv("GP_BALANCE_GRAPH", mode)
+    for mode in ("0", "full", "all", "host"):
+        monkeypatch.setenv("GP_BALANCE_GRAPH", "0" if mode == "host" else mode)
+        monkeypatch.setenv("GP_DEVICE_DECIDE", "0" if mode == "host" else "1")
         runs[mode] = balanced_kmeans_points(pts, w, s, return_stats=True)
     ref = O.run(pts, w, O.Knobs(k=k, seed=0, max_iter=10), scan_chunks=16)
     for mode, (part, stats) in runs.items():
