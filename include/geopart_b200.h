@@ -337,6 +337,16 @@ int gp_scatter_by_gid(const int32_t* a, const uint32_t* gids, int64_t n, int64_t
 int gp_gather_ranks(const int32_t* rank_by_gid, const uint32_t* gids, int64_t n, int32_t* out,
                     void* stream);
 
+/* Uniform grid over the centers for the scan's overflow walk and the walk kernel:
+ * cell of center c = clip(floor((centers[c] - lo) / h), 0, G - 1) per axis
+ * (row-major flat index), items = the centers sorted stably by cell, start[cell]
+ * = first item of the cell (G^d + 1 entries).  lo is a HOST array of d doubles.
+ * workspace: gp_center_grid_workspace_bytes(k). */
+int gp_center_grid_workspace_bytes(int k, size_t* bytes);
+int gp_center_grid(const double* centers, int k, int d, const double* lo, double h, int G,
+                   int32_t* start, int32_t* items, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
 /* ---- device-resident loops ------------------------------------------------ */
 /* A CUDA graph with one conditional WHILE node whose body is captured from the
  * work issued on `stream` between gp_loop_graph_begin and gp_loop_graph_end

@@ -89,6 +89,9 @@ _SIGS = {
                                   vp]),
     "gp_scatter_state": (C.c_int, [vp, i64, vp, vp, vp, vp, vp]),
     "gp_gather_ranks": (C.c_int, [vp, vp, i64, vp, vp]),
+    "gp_center_grid_workspace_bytes": (C.c_int, [C.c_int, C.POINTER(sz)]),
+    "gp_center_grid": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(f64), f64, C.c_int, vp, vp, vp,
+                                 sz, vp]),
     "gp_loop_graph_begin": (C.c_int, [vp, C.POINTER(vp)]),
     "gp_loop_graph_handle": (u64, [vp]),
     "gp_loop_graph_end": (C.c_int, [vp]),
@@ -138,7 +141,7 @@ KERNELS_PER_CALL = {
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
     "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 3, "gp_region_maps": 1, "gp_lb_remap": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
-    "gp_sfc_cut": 3, "gp_predict": 1, "gp_balance_decide": 1,
+    "gp_sfc_cut": 3, "gp_predict": 1, "gp_balance_decide": 1, "gp_center_grid": 3,
 }
 _launches = [0]
 calls: dict[str, int] = {}   # API calls by name (tools/kprof.py)

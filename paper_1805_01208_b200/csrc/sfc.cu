@@ -516,3 +516,89 @@ int gp_gather_ranks(const int32_t* rank_by_gid, const uint32_t* gids, int64_t n,
 }
 
 }  // extern "C"
+
+// ------------------------------------------------ center grid (scan overflow, walk)
+namespace gp {
+
+template <int D>
+__global__ void center_cells_kernel(const double* __restrict__ centers, int k, double lo0,
+                                    double lo1, double lo2, double h, int G,
+                                    uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  const double lo[3] = {lo0, lo1, lo2};
+  uint64_t flat = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    // np.clip(np.floor((centers - lo) / h), 0, G - 1)
+    double f = floor(__ddiv_rn(__dsub_rn(centers[c * D + j], lo[j]), h));
+    f = fmin(fmax(f, 0.0), (double)(G - 1));
+    flat = flat * (uint64_t)G + (uint64_t)f;
+  }
+  keys[c] = flat;
+  vals[c] = (uint32_t)c;
+}
+
+// start[cell] = first sorted position with key >= cell (lower bound), start[G^d] = k
+__global__ void cell_starts_kernel(const uint64_t* __restrict__ skeys, int k, int64_t ncell,
+                                   int32_t* __restrict__ start) {
+  const int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (cell > ncell) return;
+  int lo = 0, hi = k;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (skeys[mid] < (uint64_t)cell) lo = mid + 1;
+    else hi = mid;
+  }
+  start[cell] = lo;
+}
+
+}  // namespace gp
+
+extern "C" int gp_center_grid_workspace_bytes(int k, size_t* bytes) {
+  GP_REQUIRE(k >= 1, "gp_center_grid: k must be >= 1");
+  size_t b = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint64_t*)nullptr,
+                                                  (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                                  (uint32_t*)nullptr, k, 0, 64);
+  if (e != cudaSuccess) {
+    gp::set_error("center grid workspace query failed: %s", cudaGetErrorString(e));
+    return GP_ERR_CUDA;
+  }
+  *bytes = 2 * (size_t)k * (sizeof(uint64_t) + sizeof(uint32_t)) + ((b + 255) & ~(size_t)255) + 256;
+  return GP_OK;
+}
+
+extern "C" int gp_center_grid(const double* centers, int k, int d, const double* lo, double h,
+                              int G, int32_t* start, int32_t* items, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  GP_REQUIRE(d == 2 || d == 3, "gp_center_grid: bad d");
+  GP_REQUIRE(k >= 1 && G >= 1 && h > 0.0, "gp_center_grid: bad sizes");
+  size_t need = 0;
+  int rc = gp_center_grid_workspace_bytes(k, &need);
+  if (rc) return rc;
+  GP_REQUIRE(workspace_bytes >= need, "gp_center_grid: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  uint64_t* kin = (uint64_t*)ws;
+  uint64_t* kout = kin + k;
+  uint32_t* vin = (uint32_t*)(kout + k);
+  uint32_t* vout = vin + k;
+  void* tmp = (void*)(((uintptr_t)(vout + k) + 255) & ~(uintptr_t)255);
+  size_t tb = workspace_bytes - ((char*)tmp - ws);
+  int64_t ncell = 1;
+  for (int j = 0; j < d; ++j) ncell *= G;
+  int bits = 1;
+  while (bits < 64 && (1ull << bits) <= (unsigned long long)ncell) ++bits;
+  if (d == 2)
+    gp::center_cells_kernel<2><<<(k + 255) / 256, 256, 0, s>>>(centers, k, lo[0], lo[1], 0.0, h,
+                                                                G, kin, vin);
+  else
+    gp::center_cells_kernel<3><<<(k + 255) / 256, 256, 0, s>>>(centers, k, lo[0], lo[1], lo[2],
+                                                                h, G, kin, vin);
+  GP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, (uint32_t*)items, k, 0, bits,
+                                          s));
+  gp::cell_starts_kernel<<<(unsigned)((ncell + 1 + 255) / 256), 256, 0, s>>>(kout, k, ncell,
+                                                                             start);
+  return gp::check_launch("center_grid");
+}

@@ -477,37 +477,27 @@ class DevicePartitioner:
         self.cen_evt.record(self.stream)
 
     def _build_grid(self, centers: np.ndarray):
-        """Uniform grid over the point box holding the centers (k-sized host numpy),
-        walked by scan units whose candidate set overflows (gp_assign_args.grid_*)."""
+        """Uniform grid over the point box holding the centers (gp_center_grid on the
+        device copy of the centers), walked by scan units whose candidate set
+        overflows and by the walk kernel (gp_assign_args.grid_*)."""
         k, d = centers.shape
         lo = self.box.lo
         ext = float((self.box.hi - self.box.lo).max())
         G = int(np.ceil((k / 2.0) ** (1.0 / d)))
         G = max(1, min(G, 1024 if d == 2 else 128))
         h = ext / G * (1.0 + 1e-12) if ext > 0 else 1.0
-        cell = np.clip(np.floor((centers - lo) / h).astype(np.int64), 0, G - 1)
-        flat = cell[:, 0]
-        for j in range(1, d):
-            flat = flat * G + cell[:, j]
         ncell = G ** d
-        # pinned staging and stream-ordered async uploads (no host-device sync); a
-        # staging buffer is reused only after the copy that read it has completed
         if getattr(self, "grid_cap", (0, 0)) != (ncell, k):
             self.grid_cap = (ncell, k)
-            self.grid_h = torch.empty(ncell + 1 + k, dtype=torch.int32, pin_memory=True)
             self.grid_dev = torch.empty(ncell + 1 + k, dtype=torch.int32, device=self.device)
-            self.grid_evt = None
-        if self.grid_evt is not None:
-            self.grid_evt.synchronize()
-        hv = self.grid_h.numpy()
-        hv[0] = 0
-        np.cumsum(np.bincount(flat, minlength=ncell), out=hv[1:ncell + 1])
-        hv[ncell + 1:] = np.argsort(flat, kind="stable")
-        self.grid_dev.copy_(self.grid_h, non_blocking=True)
-        self.grid_evt = torch.cuda.Event()
-        self.grid_evt.record(self.stream)
+            gwb = N.size_query("gp_center_grid_workspace_bytes", k)
+            self.grid_ws = torch.empty(gwb, dtype=torch.uint8, device=self.device)
         self.grid_start = self.grid_dev[:ncell + 1]
         self.grid_items = self.grid_dev[ncell + 1:]
+        lo3 = (C.c_double * 3)(*[float(v) for v in lo] + [0.0] * (3 - d))
+        N.call("gp_center_grid", self.centers_d.data_ptr(), k, d, lo3, h, G,
+               self.grid_start.data_ptr(), self.grid_items.data_ptr(), self.grid_ws.data_ptr(),
+               self.grid_ws.numel(), self.sh)
         a = self.aargs
         a.grid_n, a.grid_h = G, h
         a.grid_start, a.grid_items = self.grid_start.data_ptr(), self.grid_items.data_ptr()
