@@ -370,7 +370,7 @@ int gp_loop_test_countdown(int* counter, unsigned long long handle, void* stream
  * regression, and, when the loop goes on, next[c] = cur[c] * clip(sqrt(target /
  * w_c), 1 - cap, 1 + cap) (kmeans.py:176-191 with d = 2: numpy's x ** 0.5 is
  * sqrt).  bal (doubles): [0] cap, [1] regressions, [2] best imbalance, [3] rounds
- * done, [4] error (target <= 0 or total <= 0), [5] stop, [6..7] unused, then the per-round
+ * done, [4] error (1: total <= 0, 2: target <= 0), [5] stop, [6..7] unused, then the per-round
  * imbalance, skips and distance evaluations (max_rounds each).  handle != 0:
  * sets the loop graph's condition to "run again". */
 int gp_balance_decide(const long long* red, int k, double wscale, double eps, int max_rounds,

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(1024) balance_decide_kernel(
         bal[0] = cap;
         tgt = total / (double)k;                // float(block_w.sum()) / k
         if (!(tgt > 0.0)) {
-          bal[4] = 1.0;
+          bal[4] = 2.0;
           stop = 1;
         }
       }

@@ -50,6 +50,7 @@ from .types import (
     BoundingBox,
     ClusterState,
     GeometryError,
+    GraphError,
     IterationRecord,
     KMeansSettings,
     KMeansStats,
@@ -849,6 +850,8 @@ class DevicePartitioner:
         bal = self.bal_h.numpy()
         rounds = int(bal[3])
         N._launches[0] += rounds * self.graph_kernels
+        if bal[4] == 1.0:
+            raise GraphError("total weight must be positive")
         if bal[4] != 0.0:
             raise ValueError("target weight must be positive")
         hist = [float(v) for v in bal[8:8 + rounds]]
@@ -955,6 +958,8 @@ class DevicePartitioner:
             self.bal_h[:8].copy_(self.bal[:8], non_blocking=True)
             self.stream.synchronize()
             rounds += 1
+            if bh[4] == 1.0:     # imbalance() of metrics.py:33-40
+                raise GraphError("total weight must be positive")
             if bh[4] != 0.0:
                 raise ValueError("target weight must be positive")
             if bh[5] != 0.0:    # stop (the next influences were not written)
