@@ -49,7 +49,7 @@ struct FoldLayout {
 };
 
 constexpr int RT = 256;             // run extraction: threads per tile
-constexpr int RPER = 16;            // entries per thread (4 chunks of 4)
+constexpr int RPER = 16;            // entries per thread (16 words of 32 per warp)
 constexpr int RTILE = RT * RPER;    // positions per tile
 
 static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k) {
@@ -103,8 +103,9 @@ __device__ __forceinline__ int32_t entry_key(const gp_fold_args& f, int64_t i, i
 
 // Pass 1 (streams a once): bit i of mask = entry i starts a run (its key differs from
 // its predecessor's), tiles[t] = run starts in tile t (RTILE entries).  Warp w of a
-// tile owns 512 consecutive entries as four 128-entry chunks (lane l: entries
-// 4l..4l+3 of a chunk, one coalesced 16-byte load).
+// tile owns 512 consecutive entries as 16 words of 32: lane l takes entry 32 t + l of
+// word t (coalesced 128-byte loads, all 16 issued first), so a word's run-start bits
+// are one ballot in entry order.
 __global__ void __launch_bounds__(RT) run_mark(gp_fold_args f, int64_t cnt, int64_t s0,
                                                uint32_t* __restrict__ mask,
                                                int32_t* __restrict__ tiles) {
@@ -112,60 +113,46 @@ __global__ void __launch_bounds__(RT) run_mark(gp_fold_args f, int64_t cnt, int6
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int bb = block_bits(f.k);
   const int64_t wbase = (int64_t)blockIdx.x * RTILE + (int64_t)warp * (RTILE / (RT / 32));
+  constexpr int NW = RTILE / (RT / 32) / 32;   // words per warp (16)
+  // every load first (the segment and carry computations below would otherwise
+  // keep them from being issued until their own loads return)
+  int av[NW];
+#pragma unroll
+  for (int t = 0; t < NW; ++t) {
+    const int64_t i = wbase + 32 * t + lane;
+    av[t] = i < cnt ? __ldcs(f.a + i) : -1;
+  }
+  const int aprev = (lane == 0 && wbase > 0 && wbase <= cnt) ? f.a[wbase - 1] : -1;
   int wseg = 0;
   int64_t wnext = INT64_MAX;
-  if (!f.list && wbase < cnt) {
-    wseg = segment_of(f.pos0 + wbase, f.n_global);
+  bool wuni = false;    // list mode: every entry of the warp lies in segment wseg
+  if (wbase < cnt) {
+    const int64_t p0 = f.list ? f.list[wbase] : wbase;
+    wseg = segment_of(f.pos0 + p0, f.n_global);
     wnext = wseg + 1 < GP_SEGMENTS ? ((int64_t)(wseg + 1) * f.n_global >> 8) - f.pos0 : INT64_MAX;
+    if (f.list) {   // the list is increasing: its last entry decides
+      const int64_t last = min(cnt, wbase + (int64_t)(RTILE / (RT / 32))) - 1;
+      wuni = f.list[last] < wnext;
+    }
   }
   auto key_of = [&](int64_t i, int c) -> int32_t {
     if (c < 0) return -1;
-    if (!f.list && i < wnext) return (int32_t)(((wseg - s0) << bb) | c);
+    if (f.list ? wuni : i < wnext) return (int32_t)(((wseg - s0) << bb) | c);
     return entry_key(f, i, c, s0, bb);
   };
-  int32_t carry = -2;   // key of the entry before the current chunk (lane 0's predecessor)
-  if (lane == 0 && wbase > 0 && wbase <= cnt) carry = entry_key(f, wbase - 1, f.a[wbase - 1], s0, bb);
+  int32_t carry = -2;   // key of the entry before the current word (lane 0's predecessor)
+  if (lane == 0 && wbase > 0 && wbase <= cnt) carry = entry_key(f, wbase - 1, aprev, s0, bb);
   int total = 0;
-  // all four chunks' loads first: 64 bytes per lane in flight
-  int4 va[4];
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    const int64_t e0 = wbase + 128 * h + 4 * lane;
-    if (e0 + 4 <= cnt) {
-      va[h] = __ldcs(reinterpret_cast<const int4*>(f.a + e0));
-    } else {
-      va[h].x = e0 < cnt ? f.a[e0] : -1;
-      va[h].y = e0 + 1 < cnt ? f.a[e0 + 1] : -1;
-      va[h].z = e0 + 2 < cnt ? f.a[e0 + 2] : -1;
-      va[h].w = e0 + 3 < cnt ? f.a[e0 + 3] : -1;
-    }
-  }
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    const int64_t e0 = wbase + 128 * h + 4 * lane;
-    const int av[4] = {va[h].x, va[h].y, va[h].z, va[h].w};
-    int32_t key[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) key[t] = key_of(e0 + t, av[t]);
-    int32_t prev = __shfl_up_sync(FULL, key[3], 1);
+  for (int t = 0; t < NW; ++t) {
+    const int64_t i = wbase + 32 * t + lane;
+    const int32_t key = key_of(i, av[t]);
+    int32_t prev = __shfl_up_sync(FULL, key, 1);
     if (lane == 0) prev = carry;
-    carry = __shfl_sync(FULL, key[3], 31);
-    unsigned b[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      b[t] = __ballot_sync(FULL, e0 + t < cnt && key[t] != (t == 0 ? prev : key[t - 1]));
-    total += __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]);
-    // entry 4l + t of the chunk is bit t of lane l's nibble: word w = lanes 8w..8w+7
-    if (lane < 4) {
-      unsigned word = 0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const unsigned byte = (b[t] >> (8 * lane)) & 0xffu;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) word |= ((byte >> j) & 1u) << (4 * j + t);
-      }
-      if (wbase + 128 * h < cnt) mask[(wbase + 128 * h) / 32 + lane] = word;
-    }
+    carry = __shfl_sync(FULL, key, 31);
+    const unsigned word = __ballot_sync(FULL, i < cnt && key != prev);
+    total += __popc(word);
+    if (lane == 0 && wbase + 32 * t < cnt) mask[(wbase + 32 * t) / 32] = word;
   }
   if (lane == 0) s_warp[warp] = total;
   __syncthreads();
