@@ -550,6 +550,16 @@ __global__ void __launch_bounds__(FT) fold_pipe(gp_fold_args f, const int32_t* _
   }
 }
 
+// GP_FOLD_PIPE=1: the prefetching fold for every many-pair shape (tuning switch)
+static bool pipe_all() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GP_FOLD_PIPE");
+    v = e && atoi(e) == 1;
+  }
+  return v == 1;
+}
+
 template <int D, int NC, int G, int B, bool UNIT>
 static void launch_fold_pipe(const gp_fold_args* f, int sms, const int32_t* starts,
                              const int32_t* sidx, const uint32_t* skey, const int32_t* pbeg,
@@ -801,8 +811,12 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
       else
         launch_fold_pipe<2, 4, 8, 1, false>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
     } else if (shape == 8) GP_FOLD(2, 4, 8, 1);
-    else if (shape == 0 && per >= 8 && f->wmode == GP_W_UNIT)   // measured 18% faster at C5
-      launch_fold_pipe<2, 4, 8, 1, true>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+    else if (shape == 0 && per >= 8 && (f->wmode == GP_W_UNIT || pipe_all()))
+      // measured 18% faster at C5
+      if (f->wmode == GP_W_UNIT)
+        launch_fold_pipe<2, 4, 8, 1, true>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+      else
+        launch_fold_pipe<2, 4, 8, 1, false>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
     else if (shape == 4) GP_FOLD(2, 4, 4, 2);
     else if (shape == 2) GP_FOLD(2, 4, 2, 4);
     else if (shape == 1) GP_FOLD(2, 4, 1, 8);
@@ -811,7 +825,12 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     else if (per >= 2) GP_FOLD(2, 4, 2, 4);
     else GP_FOLD(2, 4, 1, 8);
   } else {
-    if (per >= 6) GP_FOLD(3, 5, 6, 1);
+    if (per >= 6 && pipe_all()) {
+      if (f->wmode == GP_W_UNIT)
+        launch_fold_pipe<3, 5, 6, 1, true>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+      else
+        launch_fold_pipe<3, 5, 6, 1, false>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
+    } else if (per >= 6) GP_FOLD(3, 5, 6, 1);
     else if (per >= 4) GP_FOLD(3, 5, 4, 2);
     else if (per >= 2) GP_FOLD(3, 5, 2, 4);
     else GP_FOLD(3, 5, 1, 8);
