@@ -58,6 +58,32 @@ __device__ __forceinline__ void box_bounds_sq(const double* c, const double* lo,
   usq = __dmul_ru(__dmul_ru(su, inv2_hi), HI_SLACK);
 }
 
+// the two halves of box_bounds_sq (identical arithmetic), for passes needing one
+template <int D>
+__device__ __forceinline__ double box_usq(const double* c, const double* lo, const double* hi,
+                                          double inv2_hi) {
+  double su = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double du = fmax(__dsub_ru(c[j], lo[j]), __dsub_ru(hi[j], c[j]));
+    su = __fma_ru(du, du, su);
+  }
+  return __dmul_ru(__dmul_ru(su, inv2_hi), HI_SLACK);
+}
+template <int D>
+__device__ __forceinline__ double box_lsq(const double* c, const double* lo, const double* hi,
+                                          double inv2_lo) {
+  double sl = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double dl = 0.0;
+    if (c[j] < lo[j]) dl = __dsub_rd(lo[j], c[j]);
+    else if (c[j] > hi[j]) dl = __dsub_rd(c[j], hi[j]);
+    sl = __fma_rd(dl, dl, sl);
+  }
+  return __dmul_rd(__dmul_rd(sl, inv2_lo), LO_SLACK);
+}
+
 // fresh best / runner-up effective distances (b rounded up, s rounded down)
 // -> normalised float32 bounds under the current maps
 __device__ __forceinline__ void store_bounds(const gp_assign_args& p, const float4& L, int64_t q,
@@ -870,9 +896,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
     double m1 = INFINITY, m2 = INFINITY;
     for (int i = lane; i < nsrc; i += 32) {
       const int c = src ? src[i] : i;
-      double lsq, usq;
-      box_bounds_sq<D>(p.centers + c * D, lo, hi, p.inv2_lo[c], p.inv2_hi[c], lsq, usq);
-      two_min_merge(m1, m2, usq, INFINITY);
+      two_min_merge(m1, m2, box_usq<D>(p.centers + c * D, lo, hi, p.inv2_hi[c]), INFINITY);
     }
     for (int o = 16; o; o >>= 1) {
       const double b1 = __shfl_xor_sync(FULL, m1, o);
@@ -888,8 +912,7 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
       double take_lsq = 0.0;
       if (i < nsrc) {
         c = src ? src[i] : i;
-        double usq;
-        box_bounds_sq<D>(p.centers + c * D, lo, hi, p.inv2_lo[c], p.inv2_hi[c], take_lsq, usq);
+        take_lsq = box_lsq<D>(p.centers + c * D, lo, hi, p.inv2_lo[c]);
         take = take_lsq <= U;
       }
       const unsigned bal = __ballot_sync(FULL, take);
@@ -1227,9 +1250,7 @@ __global__ void __launch_bounds__(256) group_candidates_kernel(
   double m1 = INFINITY, m2 = INFINITY;
   for (int i = threadIdx.x; i < nsrc; i += blockDim.x) {
     const int c = src ? src[i] : i;
-    double lsq, usq;
-    box_bounds_sq<D>(centers + c * D, lo, hi, inv2_lo[c], inv2_hi[c], lsq, usq);
-    two_min_merge(m1, m2, usq, INFINITY);
+    two_min_merge(m1, m2, box_usq<D>(centers + c * D, lo, hi, inv2_hi[c]), INFINITY);
   }
   for (int o = 16; o; o >>= 1) {
     const double b1 = __shfl_xor_sync(FULL, m1, o);
@@ -1248,8 +1269,7 @@ __global__ void __launch_bounds__(256) group_candidates_kernel(
   int32_t* out = list + g * (int64_t)cap;
   for (int i = threadIdx.x; i < nsrc; i += blockDim.x) {
     const int c = src ? src[i] : i;
-    double lsq, usq;
-    box_bounds_sq<D>(centers + c * D, lo, hi, inv2_lo[c], inv2_hi[c], lsq, usq);
+    const double lsq = box_lsq<D>(centers + c * D, lo, hi, inv2_lo[c]);
     if (lsq <= U) {
       const int slot = atomicAdd(&s_n, 1);
       if (slot < cap) out[slot] = c;
@@ -1257,6 +1277,68 @@ __global__ void __launch_bounds__(256) group_candidates_kernel(
   }
   __syncthreads();
   if (threadIdx.x == 0) count[g] = s_n <= cap ? s_n : -1;
+}
+
+// One warp per group (sources of at most a few thousand centers, e.g. super groups
+// under a mega list): same candidate set as group_candidates_kernel, without a
+// 256-thread block and two block barriers per group.
+template <int D>
+__global__ void __launch_bounds__(256) group_candidates_warp_kernel(
+    const double* __restrict__ boxes, int64_t ngroups, int k, const double* __restrict__ centers,
+    const double* __restrict__ inv2_lo, const double* __restrict__ inv2_hi,
+    const int32_t* __restrict__ parent_list, const int32_t* __restrict__ parent_count,
+    int parent_cap, int ratio_log2, int32_t* __restrict__ list, int32_t* __restrict__ count,
+    int cap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= ngroups) return;
+  double lo[D], hi[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    lo[j] = boxes[g * 2 * D + j];
+    hi[j] = boxes[g * 2 * D + D + j];
+  }
+  if (!(lo[0] <= hi[0])) {  // empty group
+    if (lane == 0) count[g] = 0;
+    return;
+  }
+  const int32_t* src = nullptr;
+  int nsrc = k;
+  if (parent_list) {
+    const int64_t pg = g >> ratio_log2;
+    const int pc = parent_count[pg];
+    if (pc >= 0) {
+      src = parent_list + pg * (int64_t)parent_cap;
+      nsrc = pc;
+    }
+  }
+  double m1 = INFINITY, m2 = INFINITY;
+  for (int i = lane; i < nsrc; i += 32) {
+    const int c = src ? src[i] : i;
+    two_min_merge(m1, m2, box_usq<D>(centers + c * D, lo, hi, inv2_hi[c]), INFINITY);
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double b1 = __shfl_xor_sync(FULL, m1, o);
+    const double b2 = __shfl_xor_sync(FULL, m2, o);
+    two_min_merge(m1, m2, b1, b2);
+  }
+  const double U = m2;
+  int32_t* out = list + g * (int64_t)cap;
+  int n = 0;
+  for (int b = 0; b < nsrc; b += 32) {
+    const int i = b + lane;
+    bool take = false;
+    int c = 0;
+    if (i < nsrc) {
+      c = src ? src[i] : i;
+      take = box_lsq<D>(centers + c * D, lo, hi, inv2_lo[c]) <= U;
+    }
+    const unsigned bal = __ballot_sync(FULL, take);
+    const int slot = n + __popc(bal & ((1u << lane) - 1));
+    if (take && slot < cap) out[slot] = c;
+    n += __popc(bal);
+  }
+  if (lane == 0) count[g] = n <= cap ? n : -1;
 }
 
 // ------------------------------------------------------------ bound maps
@@ -1640,6 +1722,19 @@ int gp_group_candidates(const double* boxes, int64_t ngroups, int d, int k,
   GP_REQUIRE(cap >= 1 && k >= 1, "gp_group_candidates: bad sizes");
   if (ngroups <= 0) return GP_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  // short parent lists (super groups under mega / giga lists): one warp per group
+  if (parent_list && parent_cap <= 4096) {
+    const unsigned gw = (unsigned)((ngroups * 32 + 255) / 256);
+    if (d == 2)
+      group_candidates_warp_kernel<2><<<gw, 256, 0, s>>>(
+          boxes, ngroups, k, centers, inv2_lo, inv2_hi, parent_list, parent_count, parent_cap,
+          parent_ratio_log2, list, count, cap);
+    else
+      group_candidates_warp_kernel<3><<<gw, 256, 0, s>>>(
+          boxes, ngroups, k, centers, inv2_lo, inv2_hi, parent_list, parent_count, parent_cap,
+          parent_ratio_log2, list, count, cap);
+    return check_launch("group_candidates");
+  }
   if (d == 2)
     group_candidates_kernel<2><<<(unsigned)ngroups, 256, 0, s>>>(
         boxes, k, centers, inv2_lo, inv2_hi, parent_list, parent_count, parent_cap,
