@@ -184,7 +184,8 @@ __device__ __forceinline__ long long weight_units(const void* w, int64_t i, int 
 constexpr int FTH = 256;
 constexpr int FPER = 8;
 constexpr int WREG = 32 * FPER;       // entries per warp region (256)
-constexpr int FCHUNK = FTH * FPER;    // entries per CTA chunk (2048 = 8 regions)
+constexpr int RPW = 2;                // consecutive regions a warp takes per chunk
+constexpr int FCHUNK = FTH * FPER * RPW;   // entries per CTA chunk (4096 = 16 regions)
 
 struct AssignLayout {
   int64_t nchunks, nregions;
@@ -216,7 +217,7 @@ static AssignLayout assign_layout(int64_t m) {
 // completion on the stage's mbarrier), so each warp's HBM stream runs ahead of it
 // with no CTA-wide barrier; other regions (sparse lists, the tail) use direct loads.
 constexpr int FSTAGES = 2;
-constexpr int FREG_BYTES = WREG * 8;    // a (4 B) + packed (ub, lb) (4 B) per entry
+constexpr int FREG_BYTES = RPW * WREG * 8;   // a (4 B) + packed (ub, lb) (4 B) per entry
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -269,12 +270,12 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
   const int64_t fe = max(cb, min(ce, nfull));
   unsigned char* wsm = fsm + (size_t)warp * FSTAGES * FREG_BYTES;
   auto issue = [&](int64_t c, int sg) {
-    const int64_t e0 = (c * (FCHUNK / WREG) + warp) * WREG;
+    const int64_t e0 = (c * (FCHUNK / WREG) + RPW * warp) * WREG;
     unsigned char* base = wsm + (size_t)sg * FREG_BYTES;
     mbar_expect_tx(&s_bar[warp][sg], FREG_BYTES);
-    bulk_g2s(base, p.a + e0, WREG * 4, &s_bar[warp][sg]);
-    bulk_g2s(base + WREG * 4, reinterpret_cast<const unsigned*>(p.ublb) + e0, WREG * 4,
-             &s_bar[warp][sg]);
+    bulk_g2s(base, p.a + e0, RPW * WREG * 4, &s_bar[warp][sg]);
+    bulk_g2s(base + RPW * WREG * 4, reinterpret_cast<const unsigned*>(p.ublb) + e0,
+             RPW * WREG * 4, &s_bar[warp][sg]);
   };
   if (lane == 0) {
     for (int sg = 0; sg < FSTAGES; ++sg) mbar_init(&s_bar[warp][sg], 1);
@@ -287,31 +288,156 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
   int st = 0;            // ring stage of the next staged region, and its use parity
   unsigned phase = 0;
   for (int64_t c = cb; c < ce; ++c) {
-    const int reg = (int)c * (FCHUNK / WREG) + warp;   // m < 2^31: 32-bit entry math
-    const int rbase = reg * WREG + 2 * lane;
-    float4 lbp = lb_params(p, (int64_t)reg * WREG);   // one map per 2^15 entries
-    lbp.x *= binv;                                     // slope on the scaled stored lb~
-    int a[FPER], q[FPER];
-    float ub[FPER], lb[FPER];
+    const int reg0 = (int)c * (FCHUNK / WREG) + RPW * warp;   // m < 2^31: 32-bit entry math
+    float4 lbp = lb_params(p, (int64_t)reg0 * WREG);   // one map per 2^14 entries: both regions
+    lbp.x *= binv;                                      // slope on the scaled stored lb~
     const bool staged = c < fe;
-    int nvalid = FPER;
-    if (staged) {
-      mbar_wait(&s_bar[warp][st], phase);
-      const unsigned char* base = wsm + (size_t)st * FREG_BYTES;
-      const int2* as = reinterpret_cast<const int2*>(base);
-      const uint2* bs = reinterpret_cast<const uint2*>(base + WREG * 4);
+    const unsigned char* base = wsm + (size_t)st * FREG_BYTES;
+    if (staged) mbar_wait(&s_bar[warp][st], phase);
+    // block-weight runs of the kept points continue across the warp's regions
+    int run_a = -1, run2_a = -1;
+    RunW run_w = 0, run2_w = 0;
+#pragma unroll 1
+    for (int half = 0; half < RPW; ++half) {
+      const int reg = reg0 + half;
+      const int rbase = reg * WREG + 2 * lane;
+      int a[FPER], q[FPER];
+      float ub[FPER], lb[FPER];
+      int nvalid = FPER;
+      if (staged) {
+        const int2* as = reinterpret_cast<const int2*>(base) + half * (WREG / 2);
+        const uint2* bs = reinterpret_cast<const uint2*>(base + RPW * WREG * 4) + half * (WREG / 2);
+#pragma unroll
+        for (int h = 0; h < FPER / 2; ++h) {
+          const int2 av = as[h * 32 + lane];
+          const uint2 bw = bs[h * 32 + lane];
+          // raw scaled values: the bound-map slopes below carry the 1/bound_scale factor
+          const float2 b0 = bnd_raw(bw.x), b1 = bnd_raw(bw.y);
+          a[2 * h] = av.x; a[2 * h + 1] = av.y;
+          ub[2 * h] = b0.x; lb[2 * h] = b0.y;
+          ub[2 * h + 1] = b1.x; lb[2 * h + 1] = b1.y;
+          q[2 * h] = rbase + 64 * h;
+          q[2 * h + 1] = rbase + 64 * h + 1;
+        }
+      } else {
+        nvalid = 0;
+#pragma unroll
+        for (int e = 0; e < FPER; ++e) {
+          const int li = rbase + 64 * (e >> 1) + (e & 1);
+          q[e] = li < p.m ? (p.list ? p.list[li] : li) : -1;
+          nvalid += q[e] >= 0;
+          a[e] = q[e] >= 0 ? p.a[q[e]] : -1;
+          const float2 v = q[e] >= 0 ? bnd_raw(reinterpret_cast<const unsigned*>(p.ublb)[q[e]])
+                                     : make_float2(0.f, 0.f);
+          ub[e] = v.x;
+          lb[e] = v.y;
+        }
+      }
+      // skip test + block weights of the kept points.  Fast path (most lanes): all 8
+      // entries valid and in one block, so one parameter load and a branch-free skip
+      // mask.  General path: run-length weights (at most two runs per lane are held; a
+      // third, which needs three blocks among the lane's entries, goes to global memory).
+      unsigned need = 0;
+      bool same = staged && a[0] >= 0;
+#pragma unroll
+      for (int e = 1; e < FPER; ++e) same = same && a[e] == a[0];
+      if (same) {
+        float4 E = reinterpret_cast<const float4*>(p.ub_eval)[a[0]];
+        E.x *= binv;   // exact: the stored ub~ carries bound_scale
+        E.y *= binv;
+        unsigned keep = 0;
+#pragma unroll
+        for (int e = 0; e < FPER; ++e) {
+          // lb_evalf without its k == 1 test: A > 0 maps lb~ = inf to inf as well
+          const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
+          keep |= (unsigned)(ub_evalf(E, ub[e]) < lbv) << e;
+        }
+        need = keep ^ ((1u << FPER) - 1);
+        if (keep) {
+          RunW v = 0;
+          if (WM == GP_W_UNIT) {
+            v = (RunW)__popc(keep);
+          } else {
+#pragma unroll
+            for (int e = 0; e < FPER; ++e)
+              if (keep & (1u << e)) v += (RunW)weight_units<WM>(p.w, q[e], wshift);
+          }
+          if (a[0] == run_a) {
+            run_w += v;
+          } else {
+            if (run_a >= 0) {
+              if (run2_a >= 0)
+                atomicAdd((unsigned long long*)&p.block_w[run2_a], (unsigned long long)run2_w);
+              run2_a = run_a;
+              run2_w = run_w;
+            }
+            run_a = a[0];
+            run_w = v;
+          }
+        }
+      } else {
+        int ea = -1;          // block whose bound parameters E holds (runs share them)
+        float4 E = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < FPER; ++e) {
+          const bool valid = staged || q[e] >= 0;
+          const int ae = a[e];
+          if (ae >= 0 && ae != ea) {
+            E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
+            E.x *= binv;
+            E.y *= binv;
+            ea = ae;
+          }
+          const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
+          const bool skip = valid && ae >= 0 && ub_evalf(E, ub[e]) < lbv;
+          need |= (unsigned)(valid && !skip) << e;
+          if (skip) {
+            const RunW v = (RunW)weight_units<WM>(p.w, q[e], wshift);
+            if (ae == run_a) {
+              run_w += v;
+            } else {
+              if (run_a >= 0) {
+                if (run2_a >= 0)
+                  atomicAdd((unsigned long long*)&p.block_w[run2_a], (unsigned long long)run2_w);
+                run2_a = run_a;
+                run2_w = run_w;
+              }
+              run_a = ae;
+              run_w = v;
+            }
+          }
+        }
+      }
+      nskip += nvalid - __popc(need);
+      if (!__any_sync(FULL, need)) {   // nothing to rescan in this region (the common case)
+        if (lane == 0) runs[reg] = 0;
+        continue;
+      }
+      // compaction of the points to scan into the region's own slots, in entry order
+      // (entry 64h + 2l + b: ranks from two ballots per h)
+      int32_t* dst = scan + (int64_t)reg * WREG;
+      int32_t* dsa = olda + (int64_t)reg * WREG;
+      const unsigned lt = (1u << lane) - 1;
+      int cnt = 0;
 #pragma unroll
       for (int h = 0; h < FPER / 2; ++h) {
-        const int2 av = as[h * 32 + lane];
-        const uint2 bw = bs[h * 32 + lane];
-        // raw scaled values: the bound-map slopes below carry the 1/bound_scale factor
-        const float2 b0 = bnd_raw(bw.x), b1 = bnd_raw(bw.y);
-        a[2 * h] = av.x; a[2 * h + 1] = av.y;
-        ub[2 * h] = b0.x; lb[2 * h] = b0.y;
-        ub[2 * h + 1] = b1.x; lb[2 * h + 1] = b1.y;
-        q[2 * h] = rbase + 64 * h;
-        q[2 * h + 1] = rbase + 64 * h + 1;
+        const bool n0 = need & (1u << (2 * h)), n1 = need & (1u << (2 * h + 1));
+        const unsigned b0 = __ballot_sync(FULL, n0), b1 = __ballot_sync(FULL, n1);
+        int off = cnt + __popc(b0 & lt) + __popc(b1 & lt);
+        if (n0) {
+          dst[off] = q[2 * h];
+          dsa[off] = a[2 * h];  // the scan writes a only when the block changes
+          ++off;
+        }
+        if (n1) {
+          dst[off] = q[2 * h + 1];
+          dsa[off] = a[2 * h + 1];
+        }
+        cnt += __popc(b0) + __popc(b1);
       }
+      if (lane == 0) runs[reg] = cnt;
+    }
+    if (staged) {
       __syncwarp();   // the stage is consumed: refill it
       if (lane == 0 && c + FSTAGES < fe) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -321,115 +447,9 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
         st = 0;
         phase ^= 1u;
       }
-    } else {
-      nvalid = 0;
-#pragma unroll
-      for (int e = 0; e < FPER; ++e) {
-        const int li = rbase + 64 * (e >> 1) + (e & 1);
-        q[e] = li < p.m ? (p.list ? p.list[li] : li) : -1;
-        nvalid += q[e] >= 0;
-        a[e] = q[e] >= 0 ? p.a[q[e]] : -1;
-        const float2 v = q[e] >= 0 ? bnd_raw(reinterpret_cast<const unsigned*>(p.ublb)[q[e]])
-                                   : make_float2(0.f, 0.f);
-        ub[e] = v.x;
-        lb[e] = v.y;
-      }
     }
-    // skip test + block weights of the kept points.  Fast path (most lanes): all 8
-    // entries valid and in one block, so one parameter load and a branch-free skip
-    // mask.  General path: run-length weights (at most two runs per lane are held; a
-    // third, which needs three blocks among 8 entries, goes to global memory directly).
-    unsigned need = 0;
-    int run_a = -1, run2_a = -1;
-    RunW run_w = 0, run2_w = 0;
-    bool same = staged && a[0] >= 0;
-#pragma unroll
-    for (int e = 1; e < FPER; ++e) same = same && a[e] == a[0];
-    if (same) {
-      float4 E = reinterpret_cast<const float4*>(p.ub_eval)[a[0]];
-      E.x *= binv;   // exact: the stored ub~ carries bound_scale
-      E.y *= binv;
-      unsigned keep = 0;
-#pragma unroll
-      for (int e = 0; e < FPER; ++e) {
-        // lb_evalf without its k == 1 test: A > 0 maps lb~ = inf to inf as well
-        const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
-        keep |= (unsigned)(ub_evalf(E, ub[e]) < lbv) << e;
-      }
-      need = keep ^ ((1u << FPER) - 1);
-      if (keep) {
-        run_a = a[0];
-        if (WM == GP_W_UNIT) {
-          run_w = (RunW)__popc(keep);
-        } else {
-#pragma unroll
-          for (int e = 0; e < FPER; ++e)
-            if (keep & (1u << e)) run_w += (RunW)weight_units<WM>(p.w, q[e], wshift);
-        }
-      }
-    } else {
-      int ea = -1;          // block whose bound parameters E holds (runs share them)
-      float4 E = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int e = 0; e < FPER; ++e) {
-        const bool valid = staged || q[e] >= 0;
-        const int ae = a[e];
-        if (ae >= 0 && ae != ea) {
-          E = reinterpret_cast<const float4*>(p.ub_eval)[ae];
-          E.x *= binv;
-          E.y *= binv;
-          ea = ae;
-        }
-        const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
-        const bool skip = valid && ae >= 0 && ub_evalf(E, ub[e]) < lbv;
-        need |= (unsigned)(valid && !skip) << e;
-        if (skip) {
-          const RunW v = (RunW)weight_units<WM>(p.w, q[e], wshift);
-          if (ae == run_a) {
-            run_w += v;
-          } else {
-            if (run_a >= 0) {
-              if (run2_a >= 0)
-                atomicAdd((unsigned long long*)&p.block_w[run2_a], (unsigned long long)run2_w);
-              run2_a = run_a;
-              run2_w = run_w;
-            }
-            run_a = ae;
-            run_w = v;
-          }
-        }
-      }
-    }
-    nskip += nvalid - __popc(need);
     tab_add(tab, p.block_w, lane, run2_a >= 0, run2_a, run2_w);
     tab_add(tab, p.block_w, lane, run_a >= 0, run_a, run_w);
-    if (!__any_sync(FULL, need)) {   // nothing to rescan in this region (the common case)
-      if (lane == 0) runs[reg] = 0;
-      continue;
-    }
-    // compaction of the points to scan into the region's own slots, in entry order
-    // (entry 64h + 2l + b: ranks from two ballots per h)
-    int32_t* dst = scan + (int64_t)reg * WREG;
-    int32_t* dsa = olda + (int64_t)reg * WREG;
-    const unsigned lt = (1u << lane) - 1;
-    int base = 0;
-#pragma unroll
-    for (int h = 0; h < FPER / 2; ++h) {
-      const bool n0 = need & (1u << (2 * h)), n1 = need & (1u << (2 * h + 1));
-      const unsigned b0 = __ballot_sync(FULL, n0), b1 = __ballot_sync(FULL, n1);
-      int off = base + __popc(b0 & lt) + __popc(b1 & lt);
-      if (n0) {
-        dst[off] = q[2 * h];
-        dsa[off] = a[2 * h];  // the scan writes a only when the block changes
-        ++off;
-      }
-      if (n1) {
-        dst[off] = q[2 * h + 1];
-        dsa[off] = a[2 * h + 1];
-      }
-      base += __popc(b0) + __popc(b1);
-    }
-    if (lane == 0) runs[reg] = base;
   }
   for (int o = 16; o; o >>= 1) nskip += __shfl_xor_sync(FULL, nskip, o);
   if (lane == 0 && nskip) atomicAdd(&p.counters[0], nskip);
