@@ -348,8 +348,10 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
         unsigned keep = 0;
 #pragma unroll
         for (int e = 0; e < FPER; ++e) {
-          // lb_evalf without its k == 1 test: A > 0 maps lb~ = inf to inf as well
-          const float lbv = fmaxf(__fmaf_rd(lbp.x, lb[e], -lbp.y), 0.f);
+          // lb_evalf without its k == 1 test (A > 0 maps lb~ = inf to inf as well) and
+          // without its floor at 0: the evaluated ub is a sound upper bound of a
+          // distance, so it is >= 0 and "ub < lb" is unchanged by the floor
+          const float lbv = __fmaf_rd(lbp.x, lb[e], -lbp.y);
           keep |= (unsigned)(ub_evalf(E, ub[e]) < lbv) << e;
         }
         need = keep ^ ((1u << FPER) - 1);
