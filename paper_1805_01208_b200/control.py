@@ -57,6 +57,17 @@ def adapt_influence(state: ClusterState, target_weight: float, cap: float) -> Cl
     return replace(state, influence=state.influence * step)
 
 
+def row_norms(diff: np.ndarray) -> np.ndarray:
+    """np.linalg.norm(diff, axis=1) (kmeans.py:588), bit for bit: numpy reduces the
+    squared components of a row in order, sqrt((x^2 + y^2) + z^2); the explicit sum
+    avoids the slow short-axis reduction (~0.4 ms at k = 16384)."""
+    sq = diff * diff
+    s = sq[:, 0]
+    for j in range(1, diff.shape[1]):
+        s = s + sq[:, j]
+    return np.sqrt(s)
+
+
 def eroded(influence: np.ndarray, moves: np.ndarray, beta: float) -> np.ndarray:
     """kmeans.py:204-205: influence ** (1 - alpha), alpha = 2/(1+exp(-delta/beta)) - 1."""
     alpha = 2.0 / (1.0 + np.exp(-moves / beta)) - 1.0

@@ -38,6 +38,7 @@ import torch
 from . import _native as N
 from .control import (
     BoundMaps,
+    row_norms,
     imbalance,
     influence_factor,
     eroded,
@@ -726,7 +727,7 @@ class DevicePartitioner:
             safe = np.where(empty, 1.0, totals)
             new_centers = sums / safe[:, None]
             new_centers[empty] = centers[empty]
-            moves = np.linalg.norm(new_centers - centers, axis=1)
+            moves = row_norms(new_centers - centers)
             stats.iterations.append(IterationRecord(
                 phase=phase, active_points=self.m_global, balance_rounds=info.rounds,
                 imbalance=info.imbalance, skip_decisions=info.skip_decisions,

@@ -116,3 +116,16 @@ def test_sample_schedule():
 
 def test_einsum_order_probe():
     assert einsum_order3() in (0, 1, 2)
+
+
+def test_row_norms_bit_identical_to_linalg_norm():
+    import numpy as np
+
+    from paper_1805_01208_b200.control import row_norms
+
+    rng = np.random.default_rng(12)
+    for d in (2, 3):
+        for scale in (1e-9, 1.0, 1e7):
+            x = (rng.random((20_000, d)) - 0.5) * scale
+            x[:7] = 0.0
+            assert np.array_equal(row_norms(x), np.linalg.norm(x, axis=1))
