@@ -718,7 +718,12 @@ class DevicePartitioner:
                                          last_move.copy()), info.imbalance)
             # ---------------- movement (kmeans.py:585-626)
             self._fold(0)
-            red = self.fold_out.cpu().numpy()
+            if getattr(self, "fold_h", None) is None:
+                self.fold_h = torch.empty(self.fold_out.numel(), dtype=torch.float64,
+                                          pin_memory=True)
+            self.fold_h.copy_(self.fold_out, non_blocking=True)
+            self.stream.synchronize()
+            red = self.fold_h.numpy().copy()
             sums = red[:k * d].reshape(k, d)
             totals = red[k * d:k * (d + 1)]
             extents = red[k * (d + 1):k * (d + 2)]
