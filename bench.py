@@ -74,13 +74,44 @@ def load_peaks():
 def ncu_traffic(cfg):
     """DRAM bytes of one captured assign round (ncu --set full, committed under
     profiles/) next to that round's algorithmic bytes, or None."""
-    path = os.path.join(ROOT, "profiles", "round1", f"ncu_traffic_{cfg}.json")
+    path = os.path.join(ROOT, "profiles", "round2", f"ncu_traffic_{cfg}.json")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "round1", f"ncu_traffic_{cfg}.json")
     try:
         with open(path) as f:
             t = json.load(f)
         return t
     except Exception:
         return None
+
+
+def split_roofline(f_bytes, f_ms, s_bytes, s_ms, flops, world, peak, tr):
+    """Filter (skip test + block weights: n_act*(20+w_B)) and scan (rescans:
+    n_scan*(8d+20) bytes, n_eval*(3d+1) flops) separately, live CUDA-event times."""
+    out = {}
+    for name, b, ms in (("filter", f_bytes, f_ms), ("scan", s_bytes, s_ms)):
+        ach = b / world / (ms / 1e3) / 1e9 if ms > 0 else None
+        out[name] = {"alg_bytes": b / world, "ms": ms, "achieved_gbs": ach,
+                     "frac": ach / peak if ach else None,
+                     "dram": ((tr or {}).get("kernels") or {}).get(name)}
+    return out
+
+
+def fp64_roofline(flops, world, s_ms, tr):
+    """FP64 term of north_star's roofline: surviving distance evaluations x (3d+1)
+    over the scan time, against the FP64 peak measured on the box (tools/fp64_peak)."""
+    pk = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "round2", "fp64_peak.json")) as f:
+            pk = json.load(f)
+    except Exception:
+        pass
+    ach = flops / world / (s_ms / 1e3) / 1e12 if s_ms > 0 else None
+    peak = pk["tflops"] if pk else None
+    return {"alg_flops": flops / world, "achieved_tflops": ach, "peak_tflops": peak,
+            "peak_source": pk.get("how") if pk else None,
+            "frac": (ach / peak) if (ach and peak) else None,
+            "ncu": (tr or {}).get("fp64")}
 
 
 def workload(cfg):
@@ -282,6 +313,65 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+# ------------------------------------------------------------------ result gate
+def _torch_argmin(P, centers, infl, chunk=4096):
+    """Exact weighted-Voronoi argmin with the reference's per-pair fp64 arithmetic
+    (kmeans.py:157-159: diff, separately rounded squares summed in the einsum order,
+    correctly rounded sqrt and division; one eager torch op per kernel, so nothing
+    is contracted into FMA), first minimum on ties.  Independent of the product's
+    kernels."""
+    import torch
+
+    from paper_1805_01208_b200.numerics import einsum_order3
+
+    C = torch.from_numpy(np.ascontiguousarray(centers)).to(P.device)
+    f = torch.from_numpy(np.ascontiguousarray(infl)).to(P.device)
+    d = P.shape[1]
+    order = [0, 1] if d == 2 else {0: [0, 1, 2], 1: [0, 2, 1], 2: [1, 2, 0]}[einsum_order3()]
+    out = []
+    for s in range(0, P.shape[0], chunk):
+        p = P[s:s + chunk]
+        sq = []
+        for j in range(d):
+            dj = p[:, None, j] - C[None, :, j]
+            sq.append(dj * dj)
+        q = sq[order[0]] + sq[order[1]]
+        for j in order[2:]:
+            q = q + sq[j]
+        out.append(torch.argmin(torch.sqrt(q) / f[None, :], dim=1))
+    return torch.cat(out)
+
+
+def result_gate(pts_d, w_d, labels, stats, c, single):
+    """Correctness of the benchmarked partition (SURVEY §8c for C5): final imbalance
+    recomputed from the labels, the flags, and an exact-argmin audit of a random
+    2^20-point subsample of the final state."""
+    import torch
+
+    from paper_1805_01208_b200.control import imbalance
+
+    st = stats.final_state
+    out = {"final_imbalance": float(imbalance(st.block_weights)),
+           "balance_failed": bool(stats.balance_failed), "converged": bool(stats.converged),
+           "iterations": len(stats.iterations), "epsilon": c["epsilon"]}
+    if not single:
+        return out
+    n = labels.shape[0]
+    w = (torch.ones(n, dtype=torch.float64, device=labels.device) if w_d is None
+         else w_d.to(torch.float64))
+    bw = torch.zeros(c["k"], dtype=torch.float64, device=labels.device)
+    bw.index_add_(0, labels, w)
+    out["labels_block_weights_match"] = bool(np.array_equal(bw.cpu().numpy(), st.block_weights))
+    m = min(n, 1 << 20)
+    ids = torch.from_numpy(np.sort(np.random.default_rng(11).choice(n, m, replace=False)))
+    ids = ids.to(labels.device)
+    P = pts_d[ids].contiguous()
+    bad = int((_torch_argmin(P, st.centers, st.influence) != labels[ids]).sum().item())
+    out["argmin_audit"] = {"sample_points": int(m), "mismatches": bad,
+                           "checker": "torch fp64 brute force over all k (bench.py _torch_argmin)"}
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_b200(args):
     import torch
@@ -325,11 +415,15 @@ def run_b200(args):
         if dist is not None:
             dist.barrier()
 
+    last = {}
+
     def step(timer=None):
+        last.clear()   # the previous labels are released before the next partition
         if world > 1:
             a, stats = partition_distributed(pts_d, w_d, settings, device=dev, timer=timer)
         else:
             a, stats = partition_device(pts_d, w_d, settings, device=dev, timer=timer)
+        last["labels"] = a
         return stats
 
     for _ in range(args.warmup):
@@ -354,6 +448,7 @@ def run_b200(args):
         decisions += sum(r.total_decisions for r in stats.iterations)
     launches = N.launch_count()
     clk = clocks.stop()
+    result = result_gate(pts_d, w_d, last["labels"], stats, c, rows is None)
     t_total = sum(times)
     if dist is not None:
         tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
@@ -365,10 +460,16 @@ def run_b200(args):
     # roofline of the assign kernel
     wb = 0 if w_d is None else 8
     alg_bytes, kern_ms, flops = 0.0, 0.0, 0.0
+    f_bytes, s_bytes, f_ms, s_ms = 0.0, 0.0, 0.0, 0.0
     for timer, stats in timers:
         kern_ms += timer.total_ms()
+        fm, sm = timer.split_ms()
+        f_ms += fm
+        s_ms += sm
         for (nact, nscan, nev) in timer.rounds:
             alg_bytes += nact * (4 + 16 + wb) + nscan * (8 * d + 20)
+            f_bytes += nact * (4 + 16 + wb)
+            s_bytes += nscan * (8 * d + 20)
             flops += nev * (3 * d + 1)
     launches_assign = sum(len(t.events) for t, _ in timers)
     peak, peak_kind = load_peaks()
@@ -437,7 +538,13 @@ def run_b200(args):
                          "avg_launch_us": kern_ms * 1e3 / max(launches_assign, 1),
                          "alg_bytes_per_launch": alg_bytes / max(launches_assign, 1),
                          "fp64_flops_per_launch": flops / max(launches_assign, 1),
-                         "kernel_share_of_step": kern_ms / 1e3 / t_total},
+                         "kernel_share_of_step": kern_ms / 1e3 / t_total,
+                         # the two launches of every round, each on its own §8d bytes
+                         "split": split_roofline(f_bytes, f_ms, s_bytes, s_ms, flops, world,
+                                                 peak, tr),
+                         "frac_dram": (tr or {}).get("frac_dram"),
+                         "fp64": fp64_roofline(flops, world, s_ms, tr)},
+            "result": result,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches // max(args.steps, 1) if launches else None,

@@ -195,6 +195,9 @@ typedef struct gp_assign_args {
   /* device copy of inv2_min kept by gp_update_maps (map_state + 2k + 7); when set it
    * replaces inv2_min, so a captured loop graph sees every round's value */
   const double* inv2_min_dev;
+  /* optional cudaEvent_t recorded on the stream between the filter and the scan
+   * launches (per-kernel timing); NULL: none */
+  void* split_event;
 } gp_assign_args;
 int gp_assign_workspace_bytes(int64_t m, size_t* bytes);
 int gp_assign_round(const gp_assign_args* args, void* stream);
@@ -347,23 +350,9 @@ int gp_center_grid(const double* centers, int k, int d, const double* lo, double
                    int32_t* start, int32_t* items, void* workspace, size_t workspace_bytes,
                    void* stream);
 
-/* ---- device-resident loops ------------------------------------------------ */
-/* A CUDA graph with one conditional WHILE node whose body is captured from the
- * work issued on `stream` between gp_loop_graph_begin and gp_loop_graph_end
- * (stream capture into the body graph).  A body kernel decides whether the loop
- * runs again (cudaGraphSetConditional on gp_loop_graph_handle(ctx)).  Used for
- * the balance rounds of one movement iteration (kmeans.py:415-443): the host
- * launches the whole loop and synchronises once.  gp_loop_test_countdown is a
- * body kernel for tests: --*counter, loop while it is positive. */
-int gp_loop_graph_begin(void* stream, void** ctx);
-unsigned long long gp_loop_graph_handle(void* ctx);
-int gp_loop_graph_end(void* ctx);
-int gp_loop_graph_launch(void* ctx, void* stream);
-int gp_loop_graph_destroy(void* ctx);
-int gp_loop_test_countdown(int* counter, unsigned long long handle, void* stream);
-
+/* ---- device-side balance decision ----------------------------------------- */
 /* One balance-round decision of assign_and_balance (kmeans.py:425-443) on the
- * device, for the loop graph (d = 2, exact block weights): from the round's
+ * device (d = 2, exact block weights): from the round's
  * block-weight units and counters red[k + 3] (gp_assign_round), the block
  * weights units / wscale, imbalance (metrics.py:33-40), the stop test
  * (imbalance <= eps or the last round), the step halving from the second
@@ -371,11 +360,9 @@ int gp_loop_test_countdown(int* counter, unsigned long long handle, void* stream
  * w_c), 1 - cap, 1 + cap) (kmeans.py:176-191 with d = 2: numpy's x ** 0.5 is
  * sqrt).  bal (doubles): [0] cap, [1] regressions, [2] best imbalance, [3] rounds
  * done, [4] error (1: total <= 0, 2: target <= 0), [5] stop, [6..7] unused, then the per-round
- * imbalance, skips and distance evaluations (max_rounds each).  handle != 0:
- * sets the loop graph's condition to "run again". */
+ * imbalance, skips and distance evaluations (max_rounds each). */
 int gp_balance_decide(const long long* red, int k, double wscale, double eps, int max_rounds,
-                      double* bal, const double* infl_cur, double* infl_next,
-                      unsigned long long handle, void* stream);
+                      double* bal, const double* infl_cur, double* infl_next, void* stream);
 
 /* ---- callers of the path ---------------------------------- */
 

@@ -421,6 +421,22 @@ def brute_labels(points, centers, infl):
     return arg
 
 
+def brute_labels_blocked(points, centers, infl, block=256):
+    """brute_labels for large k: effdist's exact arithmetic (kmeans.py:157-159,
+    the same einsum over rows of diff) on (block x k) tiles; np.argmin keeps the
+    first (lowest-index) minimum, the reference's tie-break."""
+    points = np.asarray(points, dtype=np.float64)
+    n, d = points.shape
+    k = centers.shape[0]
+    out = np.empty(n, dtype=np.int64)
+    for s in range(0, n, block):
+        p = points[s:s + block]
+        diff = (p[:, None, :] - centers[None, :, :]).reshape(-1, d)
+        dist = np.sqrt(np.einsum("ij,ij->i", diff, diff)).reshape(p.shape[0], k) / infl[None, :]
+        out[s:s + block] = np.argmin(dist, axis=1)
+    return out
+
+
 def runner_up_gap(points, centers, infl):
     """Relative gap between the best and second-best effective distance per point."""
     mat = np.stack([effdist(points, centers[c], infl[c]) for c in range(centers.shape[0])], axis=1)

@@ -35,6 +35,7 @@ class AssignArgs(C.Structure):
         ("grid_start", vp), ("grid_items", vp), ("grid_lo", f64 * 3), ("grid_h", f64),
         ("inv2_min", f64), ("unit_boxes", vp), ("unit_shift", i32), ("flags", i32),
         ("lb_rpar", vp), ("lb_rshift", i32), ("bound_scale", C.c_float), ("inv2_min_dev", vp),
+        ("split_event", vp),
     ]
 
 
@@ -92,13 +93,7 @@ _SIGS = {
     "gp_center_grid_workspace_bytes": (C.c_int, [C.c_int, C.POINTER(sz)]),
     "gp_center_grid": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(f64), f64, C.c_int, vp, vp, vp,
                                  sz, vp]),
-    "gp_loop_graph_begin": (C.c_int, [vp, C.POINTER(vp)]),
-    "gp_loop_graph_handle": (u64, [vp]),
-    "gp_loop_graph_end": (C.c_int, [vp]),
-    "gp_loop_graph_launch": (C.c_int, [vp, vp]),
-    "gp_loop_graph_destroy": (C.c_int, [vp]),
-    "gp_loop_test_countdown": (C.c_int, [vp, u64, vp]),
-    "gp_balance_decide": (C.c_int, [vp, C.c_int, f64, f64, C.c_int, vp, vp, vp, u64, vp]),
+    "gp_balance_decide": (C.c_int, [vp, C.c_int, f64, f64, C.c_int, vp, vp, vp, vp]),
     "gp_sfc_cut_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_sfc_cut": (C.c_int, [vp, vp, i64, C.c_int, f64, vp, vp, sz, vp]),
     "gp_predict": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]),

@@ -8,6 +8,7 @@ same numpy operations in the same order.  Nothing here touches per-point data.
 
 from __future__ import annotations
 
+import functools
 import math
 from dataclasses import replace
 
@@ -57,15 +58,34 @@ def adapt_influence(state: ClusterState, target_weight: float, cap: float) -> Cl
     return replace(state, influence=state.influence * step)
 
 
-def row_norms(diff: np.ndarray) -> np.ndarray:
-    """np.linalg.norm(diff, axis=1) (kmeans.py:588), bit for bit: numpy reduces the
-    squared components of a row in order, sqrt((x^2 + y^2) + z^2); the explicit sum
-    avoids the slow short-axis reduction (~0.4 ms at k = 16384)."""
+@functools.lru_cache(maxsize=None)
+def _norm_order_is_sequential() -> bool:
+    """Does this host's np.linalg.norm(axis=1) sum a row's squares left to right?
+    (numpy's iterator / SIMD paths decide it; probed once per process.)"""
+    rng = np.random.default_rng(4321)
+    out = True
+    for d in (2, 3):
+        x = (rng.random((20000, d)) - 0.5) * rng.uniform(1e-3, 1e3, (20000, 1))
+        out = out and np.array_equal(np.linalg.norm(x, axis=1), _row_norms_seq(x))
+    return bool(out)
+
+
+def _row_norms_seq(diff: np.ndarray) -> np.ndarray:
     sq = diff * diff
     s = sq[:, 0]
     for j in range(1, diff.shape[1]):
         s = s + sq[:, j]
     return np.sqrt(s)
+
+
+def row_norms(diff: np.ndarray) -> np.ndarray:
+    """np.linalg.norm(diff, axis=1) (kmeans.py:588), bit for bit: numpy reduces the
+    squared components of a row in order, sqrt((x^2 + y^2) + z^2); the explicit sum
+    avoids the slow short-axis reduction (~0.4 ms at k = 16384).  Where a probe finds
+    this host's numpy summing in another order, np.linalg.norm itself is used."""
+    if not _norm_order_is_sequential():
+        return np.linalg.norm(diff, axis=1)
+    return _row_norms_seq(diff)
 
 
 def eroded(influence: np.ndarray, moves: np.ndarray, beta: float) -> np.ndarray:

@@ -1561,13 +1561,18 @@ static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout
   }
   unsigned gf = persistent_grid((const void*)filter_kernel<WM>, FTH, L.nchunks, fsm);
   filter_kernel<WM><<<gf, FTH, fsm, s>>>(*a, wshift, L.nchunks, scan, olda, runs, sched);
+  if (a->split_event) cudaEventRecord((cudaEvent_t)a->split_event, s);
   if (g_sreg == 0) {
     const char* e = getenv("GP_SCAN_REGIONS");
     g_sreg = e ? atoi(e) : -1;
   }
   // dense (full-phase) lists: 4 regions per scan unit; sparse sample lists: 1
-  int sreg = g_sreg > 0 ? g_sreg
-                       : (a->scan_regions > 0 ? a->scan_regions : (a->list ? 1 : SREG));
+  int sreg = a->scan_regions > 0 ? a->scan_regions : (a->list ? 1 : SREG);
+  // the tuning override may only change the unit when no per-unit boxes (sized for
+  // scan_regions) or group lists (sized for at least one unit) depend on it
+  if (g_sreg > 0 && !a->unit_boxes &&
+      (!a->group_list || (int64_t)g_sreg * WREG <= (1ll << a->group_shift)))
+    sreg = g_sreg;
   if (sreg > SREG) sreg = SREG;
   // consecutive units per claim only when there are many more units than warps (few,
   // heavy units of a small warm-up sample go one per warp)

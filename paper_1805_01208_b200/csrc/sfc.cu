@@ -344,7 +344,7 @@ using namespace gp;
 extern "C" {
 
 const char* gp_last_error(void) { return g_err; }
-int gp_abi_version(void) { return 1; }
+int gp_abi_version(void) { return 2; }
 void gp_args_sizes(size_t* a, size_t* f) {
   *a = sizeof(gp_assign_args);
   *f = sizeof(gp_fold_args);

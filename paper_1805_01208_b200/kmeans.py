@@ -102,6 +102,7 @@ class _Timer:
 
     def __init__(self):
         self.events = []
+        self.mids = []
         self.rounds = []   # (n_active, n_scanned, n_evals) per assign launch
         self.scan = []     # gp_scan_stats per round (GP_SCAN_STATS=1)
 
@@ -110,9 +111,29 @@ class _Timer:
         ev.record(stream)
         return ev
 
+    def begin(self, stream, aargs):
+        """Events around one gp_assign_round, plus one the library records between
+        its filter and scan launches (gp_assign_args.split_event)."""
+        e0 = self.mark(stream)
+        mid = self.mark(stream)          # recorded once so the CUDA event exists
+        aargs.split_event = mid.cuda_event
+        return e0, mid
+
+    def end(self, stream, aargs, tok):
+        aargs.split_event = None
+        self.events.append((tok[0], self.mark(stream)))
+        self.mids.append(tok[1])
+
     def total_ms(self) -> float:
         torch.cuda.synchronize()
         return sum(a.elapsed_time(b) for a, b in self.events)
+
+    def split_ms(self) -> tuple[float, float]:
+        """(filter, scan) milliseconds summed over the assign rounds."""
+        torch.cuda.synchronize()
+        f = sum(a.elapsed_time(m) for (a, _), m in zip(self.events, self.mids))
+        s = sum(m.elapsed_time(b) for (_, b), m in zip(self.events, self.mids))
+        return f, s
 
 
 def sample_ranks_device(n: int, seed: int, device, stream) -> torch.Tensor:
@@ -265,10 +286,19 @@ class DevicePartitioner:
             raise GeometryError("points must be an (n, d) array")
         w = None
         if weights is not None:
+            n = pts.shape[0]
+            shape = tuple(weights.shape) if hasattr(weights, "shape") else np.shape(weights)
+            if len(shape) != 1:
+                raise ValueError(f"weights must be a 1-D array of length {n}, got shape {shape}")
+            if shape[0] < n:
+                # the reference fails in its redistribution gather (ranksim.py:160-168)
+                raise IndexError(f"weights has {shape[0]} entries for {n} points")
             if isinstance(weights, torch.Tensor):
-                w = weights.to(device=dev, dtype=torch.float64).contiguous()
+                w = weights[:n].to(device=dev, dtype=torch.float64).contiguous()
             else:
-                w = torch.from_numpy(np.ascontiguousarray(np.asarray(weights, dtype=np.float64)))
+                # extra entries are ignored, as the reference's shard slices do
+                # (ranksim.py:101-106)
+                w = torch.from_numpy(np.ascontiguousarray(np.asarray(weights, dtype=np.float64)[:n]))
                 w = w.to(dev)
         return pts, w
 
@@ -628,11 +658,11 @@ class DevicePartitioner:
         self.lists_fresh = False
         self.red.zero_()
         if self.timer is not None:
-            e0 = self.timer.mark(self.stream)
+            tok = self.timer.begin(self.stream, self.aargs)
         N.count("gp_assign_round")
         N.check(N.lib.gp_assign_round(C.byref(self.aargs), self.sh), "gp_assign_round")
         if self.timer is not None:
-            self.timer.events.append((e0, self.timer.mark(self.stream)))
+            self.timer.end(self.stream, self.aargs, tok)
         self._reduce_round()
         self.red_h.copy_(self.red, non_blocking=True)
         self.stream.synchronize()
@@ -703,9 +733,7 @@ class DevicePartitioner:
             if phase == "full" and self.hier is not None and self.rmaps is None:
                 self._enter_region_maps(infl)
             # ---------------- assign_and_balance (kmeans.py:377-453)
-            if self._graph_ok():
-                info, infl = self._balance_graph(infl)
-            elif self._device_decide_ok():
+            if self._device_decide_ok():
                 info, infl = self._balance_device(infl)
             else:
                 info, infl = self._balance_host(infl)
@@ -785,134 +813,11 @@ class DevicePartitioner:
         self.release()
         return out, stats
 
-    # ------------------------------------------------------------ loop graphs
-    def _graph_ok(self) -> bool:
-        """The balance rounds can run as one device-resident loop graph when every
-        decision of the round is reproducible on the device: d = 2 (the influence
-        step is a sqrt), exact integer block weights, one GPU, no audit or
-        per-round statistics.  Opt-in (GP_BALANCE_GRAPH=full|all): measured slower
-        than the host-driven rounds this round."""
-        mode = os.environ.get("GP_BALANCE_GRAPH", "0")
-        if mode == "0" or not (type(self) is DevicePartitioner and self.d == 2
-                               and self.wplan.exact and not self.settings.audit_bounds
-                               and not (self.aargs.flags & 1)):
-            return False
-        # a warm-up sample step has a new active set (a new capture) and ~20 short
-        # rounds: capturing there costs more than it saves, so by default only the
-        # full phase, whose iterations all share one graph, uses it ("all": every phase)
-        return mode == "all" or (self.aargs.list is None and not getattr(self, "dense_m", 0))
-
-    def _balance_graph(self, infl):
-        """assign_and_balance (kmeans.py:377-453) as a CUDA graph with a conditional
-        WHILE node: each pass applies the previous pass's influence step (bound maps,
-        candidate lists, region maps; the identity on the first pass), runs the
-        assign round and decides on the device (gp_balance_decide) whether to go on.
-        The host launches the loop once and reads the per-round records after it."""
-        st, k, a = self.settings, self.settings.k, self.aargs
-        mr = st.max_balance_iter
-        if getattr(self, "bal", None) is None or self.bal.numel() < 8 + 3 * mr:
-            self.bal = torch.empty(8 + 3 * mr, dtype=torch.float64, device=self.device)
-            self.bal_h = torch.empty(8 + 3 * mr, dtype=torch.float64, pin_memory=True)
-            self.bal_init = torch.empty(8, dtype=torch.float64, pin_memory=True)
-            self.loop_graphs = {}
-        cur, nxt = self.cur, 1 - self.cur
-        cur_p, nxt_p = self._infl_ptr(cur), self._infl_ptr(nxt)
-        key = (cur, a.X, a.a, a.ublb, a.list, a.m, a.flags, a.scan_regions, a.unit_boxes,
-               a.unit_shift, a.lb_rpar, a.group_list, a.group_count, a.grid_start, a.grid_n,
-               self.rmaps, self.walk, getattr(self.hier, "key", None), mr, st.epsilon,
-               self.wplan.scale, a.workspace)
-        ctx = self.loop_graphs.get(key)
-        if ctx is None:
-            for old in self.loop_graphs.values():
-                N.lib.gp_loop_graph_destroy(old)
-            self.loop_graphs = {}
-            # capture on a side stream (the legacy default stream cannot capture);
-            # the graph itself is launched on the partition's stream
-            if getattr(self, "cap_stream", None) is None:
-                self.cap_stream = torch.cuda.Stream(self.device)
-            self.cap_stream.wait_stream(self.stream)
-            sh = self.sh
-            self.sh = self.cap_stream.cuda_stream
-            try:
-                with torch.cuda.stream(self.cap_stream):
-                    ctx = self._capture_balance_graph(cur_p, nxt_p)
-            finally:
-                self.sh = sh
-            self.loop_graphs[key] = ctx
-        # loop state: cap, regressions, best imbalance, rounds, error; next := cur so
-        # the first pass's influence step is the identity
-        self.bal_init.numpy()[:] = [st.influence_step_cap, 0.0, math.inf, 0.0, 0.0, 0.0, 0.0, 0.0]
-        self.bal[:8].copy_(self.bal_init, non_blocking=True)
-        self.kstate[nxt * k:(nxt + 1) * k].copy_(self.kstate[cur * k:(cur + 1) * k])
-        if self.timer is not None:
-            e0 = self.timer.mark(self.stream)
-        N.count("gp_assign_round")
-        N.check(N.lib.gp_loop_graph_launch(ctx, self.sh), "gp_loop_graph_launch")
-        if self.timer is not None:
-            self.timer.events.append((e0, self.timer.mark(self.stream)))
-        self.red_h.copy_(self.red, non_blocking=True)
-        self.bal_h.copy_(self.bal, non_blocking=True)
-        self.stream.synchronize()
-        bal = self.bal_h.numpy()
-        rounds = int(bal[3])
-        N._launches[0] += rounds * self.graph_kernels
-        if bal[4] == 1.0:
-            raise GraphError("total weight must be positive")
-        if bal[4] != 0.0:
-            raise ValueError("target weight must be positive")
-        hist = [float(v) for v in bal[8:8 + rounds]]
-        skips_r = bal[8 + mr:8 + mr + rounds].astype(np.int64)
-        evals_r = bal[8 + 2 * mr:8 + 2 * mr + rounds].astype(np.int64)
-        blk = self.red_h.numpy()[:k].copy()
-        block_w = self._block_weights(blk)
-        if rounds > 1:   # the influences the last round used
-            infl = self.kstate[cur * k:(cur + 1) * k].cpu().numpy().copy()
-            a.inv2_min = 1.0 / float(np.max(infl)) ** 2 * (1.0 - 1e-15)
-        if self.timer is not None:
-            for sk, ev in zip(skips_r, evals_r):
-                self.timer.rounds.append((self.m_global, int(self.m_global - sk), int(ev)))
-        self.lists_fresh = False
-        info = BalanceInfo(rounds, hist[-1], block_w, int(skips_r.sum()),
-                           rounds * self.m_global, int(evals_r.sum()), hist)
-        return info, infl
-
-    def _capture_balance_graph(self, cur_p, nxt_p):
-        k, a, sh = self.settings.k, self.aargs, self.sh
-        ctx = C.c_void_p()
-        c0 = N.launch_count()
-        N.check(N.lib.gp_loop_graph_begin(sh, C.byref(ctx)), "gp_loop_graph_begin")
-        try:
-            handle = N.lib.gp_loop_graph_handle(ctx)
-            # the previous pass's influence step (kmeans.py:437-443): maps cur -> next,
-            # candidate lists and region maps under the new influences, then next -> cur
-            mb = self.kmaps.data_ptr()
-            N.call("gp_update_maps", cur_p, nxt_p, None, k, self.mapstate.data_ptr(),
-                   a.inv2_lo, a.inv2_hi, mb, mb + 16 * k, mb + 32 * k, self.mapflag.data_ptr(),
-                   0, self.scale_hint, sh)
-            if self.rmaps is not None:
-                self._relax_regions(cur_p, nxt_p, None, False)
-            elif self.hier is not None and not self.walk:
-                self.hier.refresh()
-            cur_t = self.kstate[self.cur * k:(self.cur + 1) * k]
-            nxt_t = self.kstate[(1 - self.cur) * k:(2 - self.cur) * k]
-            cur_t.copy_(nxt_t)
-            # the round (kmeans.py:415-425) and its decision (kmeans.py:426-443)
-            self.red.zero_()
-            N.check(N.lib.gp_assign_round(C.byref(a), sh), "gp_assign_round")
-            N.call("gp_balance_decide", self.red.data_ptr(), k, float(self.wplan.scale),
-                   float(self.settings.epsilon), self.settings.max_balance_iter,
-                   self.bal.data_ptr(), cur_p, nxt_p, handle, sh)
-        finally:
-            N.check(N.lib.gp_loop_graph_end(ctx), "gp_loop_graph_end")
-        # kernels per pass (the captured calls did not launch anything yet)
-        self.graph_kernels = N.launch_count() - c0 + 3   # + zero_, copy, assign round
-        N._launches[0] = c0
-        return ctx
-
     def _device_decide_ok(self) -> bool:
-        """Same conditions as the loop graph: the round's decision and influence step
-        run on the device (gp_balance_decide) and the host only reads a few scalars
-        per round.  GP_DEVICE_DECIDE=0 turns it off."""
+        """d = 2 (the influence step is a sqrt), exact integer block weights, no audit
+        or per-round scan statistics: the round's decision and influence step run on
+        the device (gp_balance_decide) and the host only reads a few scalars per
+        round.  GP_DEVICE_DECIDE=0 turns it off."""
         return (type(self) is DevicePartitioner and self.d == 2 and self.wplan.exact
                 and not self.settings.audit_bounds and not (self.aargs.flags & 1)
                 and os.environ.get("GP_DEVICE_DECIDE", "1") != "0")
@@ -930,7 +835,6 @@ class DevicePartitioner:
             self.bal = torch.empty(8 + 3 * mr, dtype=torch.float64, device=self.device)
             self.bal_h = torch.empty(8 + 3 * mr, dtype=torch.float64, pin_memory=True)
             self.bal_init = torch.empty(8, dtype=torch.float64, pin_memory=True)
-            self.loop_graphs = {}
         cur, nxt = self.cur, 1 - self.cur
         cur_p, nxt_p = self._infl_ptr(cur), self._infl_ptr(nxt)
         cur_t = self.kstate[cur * k:(cur + 1) * k]
@@ -954,13 +858,13 @@ class DevicePartitioner:
             self.lists_fresh = False
             self.red.zero_()
             if self.timer is not None:
-                e0 = self.timer.mark(self.stream)
+                tok = self.timer.begin(self.stream, a)
             N.count("gp_assign_round")
             N.check(N.lib.gp_assign_round(C.byref(a), self.sh), "gp_assign_round")
             if self.timer is not None:
-                self.timer.events.append((e0, self.timer.mark(self.stream)))
+                self.timer.end(self.stream, a, tok)
             N.call("gp_balance_decide", self.red.data_ptr(), k, float(self.wplan.scale),
-                   float(st.epsilon), mr, self.bal.data_ptr(), cur_p, nxt_p, 0, self.sh)
+                   float(st.epsilon), mr, self.bal.data_ptr(), cur_p, nxt_p, self.sh)
             self.bal_h[:8].copy_(self.bal[:8], non_blocking=True)
             self.stream.synchronize()
             rounds += 1
@@ -1048,9 +952,6 @@ class DevicePartitioner:
 
     def release(self):
         """Drop every n-sized device buffer (the caller keeps only the result)."""
-        for ctx in getattr(self, "loop_graphs", {}).values():
-            N.lib.gp_loop_graph_destroy(ctx)
-        self.loop_graphs = {}
         for name in ("X", "W", "A", "UBLB", "A_d", "UBLB_d", "X_d", "W_d", "gids", "rank_sfc", "active_idx",
                      "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier", "grid_start",
                      "grid_items", "ubox", "rstate", "rpar"):
@@ -1094,6 +995,18 @@ class DistributedPartitioner(DevicePartitioner):
         pts, w = self._input(points, weights)
         n_in, d = pts.shape
         self.d = d
+        # local argument errors are agreed on before any other collective, so every rank
+        # raises the same error instead of one rank leaving the others blocked
+        chk = torch.tensor([1 if n_in < 1 else 0, 1 if w is None else 0, 1 if w is not None else 0,
+                            d], dtype=torch.int64, device=self.device)
+        mx = comm.allreduce(chk.clone(), P.dist.ReduceOp.MAX).cpu().tolist()
+        mn = comm.allreduce(chk.clone(), P.dist.ReduceOp.MIN).cpu().tolist()
+        if mx[0]:
+            raise ValueError("every rank needs at least one point")
+        if mx[1] and mx[2]:
+            raise ValueError("weights must be given on every rank or on none")
+        if mx[3] != mn[3]:
+            raise GeometryError("all ranks must pass points of the same dimension")
         off, n = P.input_offsets(n_in, comm)
         self.in_offset, self.n_in = off, n_in
         k = st.k
@@ -1104,8 +1017,6 @@ class DistributedPartitioner(DevicePartitioner):
             raise GeometryError(f"unsupported dimension {d}")
         if d * depth > 62:
             raise GeometryError(f"depth {depth} out of range for dimension {d}")
-        if n_in < 1:
-            raise ValueError("every rank needs at least one point")
         self.key_bits = d * depth
         dev, sh = self.device, self.sh
         sp, sd = pts.stride()
@@ -1181,8 +1092,7 @@ class DistributedPartitioner(DevicePartitioner):
         self.comm.allreduce(has, P.dist.ReduceOp.MAX)
         if float(has.item()) == 0.0:
             return _WeightPlan(0, True, 1.0)
-        if w is None:
-            raise ValueError("weights must be given on every rank or on none")
+        assert w is not None   # agreed in bootstrap()
         out = torch.empty(3, dtype=torch.int64, device=self.device)
         N.call("gp_weight_probe", w.data_ptr(), n_in, out.data_ptr(), self.sh)
         fl, low, mxb = (int(v) for v in out.cpu().tolist())
@@ -1318,5 +1228,8 @@ def balanced_kmeans(graph, settings: KMeansSettings, world: RankWorld | None = N
         world = RankWorld.from_graph(graph)
     elif world.n != graph.n:
         raise ValueError("world does not match the graph")
-    assign_dev, stats = partition_device(graph.coords, graph.vertex_weights, settings)
-    return _finish(assign_dev, stats, settings.k, return_stats)
+    # the reference runs the pipeline on the world's own shards (kmeans.py:531-534), so a
+    # world built from other coordinates or weights (same n) partitions those
+    coords = world.coords if world.coords is not None else graph.coords
+    return balanced_kmeans_points(coords, world.weights, settings, p=world.p,
+                                  return_stats=return_stats)

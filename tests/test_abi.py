@@ -46,7 +46,7 @@ def test_library_exports_every_declared_symbol(native):
 
 
 def test_abi_version(native):
-    assert native.lib.gp_abi_version() == 1
+    assert native.lib.gp_abi_version() == 2
 
 
 def test_struct_layouts_match_header(native):

@@ -1,5 +1,4 @@
-"""Device-resident loop graphs (gp_loop_graph_*): a conditional WHILE node whose
-body is captured from stream work runs until a body kernel stops it."""
+"""Device-side balance decisions (gp_balance_decide) and the device center grid."""
 import ctypes
 
 import pytest
@@ -15,39 +14,11 @@ def _need_gpu():
         pytest.fail("CUDA device required for -m gpu tests")
 
 
-def test_while_graph_countdown():
-    import torch
-
-    from paper_1805_01208_b200 import _native as N
-
-    s = torch.cuda.Stream()
-    cnt = torch.tensor([7], dtype=torch.int32, device="cuda")
-    hits = torch.zeros(1, dtype=torch.int32, device="cuda")
-    torch.cuda.synchronize()
-    ctx = ctypes.c_void_p()
-    N.check(N.lib.gp_loop_graph_begin(s.cuda_stream, ctypes.byref(ctx)), "begin")
-    h = N.lib.gp_loop_graph_handle(ctx)
-    with torch.cuda.stream(s):
-        hits.add_(1)                       # torch work is captured into the body too
-    N.check(N.lib.gp_loop_test_countdown(cnt.data_ptr(), h, s.cuda_stream), "countdown")
-    N.check(N.lib.gp_loop_graph_end(ctx), "end")
-    for rep in range(2):
-        cnt.fill_(7 + rep)
-        hits.zero_()
-        torch.cuda.synchronize()
-        N.check(N.lib.gp_loop_graph_launch(ctx, s.cuda_stream), "launch")
-        s.synchronize()
-        assert int(cnt.item()) == 0
-        assert int(hits.item()) == 7 + rep
-    N.lib.gp_loop_graph_destroy(ctx)
-
-
 @pytest.mark.parametrize("k,weights", [(16, None), (300, "int")])
-def test_balance_graph_modes_bit_identical(monkeypatch, k, weights):
-    """The balance-round drivers (loop graph in every phase or the full phase only,
-    host loop with on-device decisions, host loop with host numpy decisions) give
-    the same partition, state and per-iteration records bit for bit, and the
-    oracle's."""
+def test_balance_drivers_bit_identical(monkeypatch, k, weights):
+    """The balance-round drivers (host loop with on-device decisions, host loop with
+    host numpy decisions) give the same partition, state and per-iteration records
+    bit for bit, and the oracle's."""
     import numpy as np
 
     from oracle import geographer_oracle as O
@@ -58,8 +29,7 @@ def test_balance_graph_modes_bit_identical(monkeypatch, k, weights):
     w = rng.integers(1, 7, 40_000).astype(float) if weights else None
     s = KMeansSettings(k=k, seed=0, max_iter=10)
     runs = {}
-    for mode in ("0", "full", "all", "host"):
-        monkeypatch.setenv("GP_BALANCE_GRAPH", "0" if mode == "host" else mode)
+    for mode in ("0", "host"):
         monkeypatch.setenv("GP_DEVICE_DECIDE", "0" if mode == "host" else "1")
         runs[mode] = balanced_kmeans_points(pts, w, s, return_stats=True)
     ref = O.run(pts, w, O.Knobs(k=k, seed=0, max_iter=10), scan_chunks=16)
@@ -97,7 +67,7 @@ def test_balance_decide_matches_host_numpy():
         units[rng.integers(0, k)] = 0                          # an empty block
         red = torch.from_numpy(np.concatenate([units, [11, 22, 33]])).cuda()
         N.check(N.lib.gp_balance_decide(red.data_ptr(), k, scale, eps, mr, bal.data_ptr(),
-                                        cur.data_ptr(), nxt.data_ptr(), 0, None), "decide")
+                                        cur.data_ptr(), nxt.data_ptr(), None), "decide")
         torch.cuda.synchronize()
         b = bal.cpu().numpy()
         bw = units.astype(np.float64) / scale
