@@ -40,6 +40,22 @@ print("API calls:", dict(sorted(N0.calls.items())))
 print(f"{'kernel':72s} {'calls':>6s} {'ms':>10s} {'%':>6s}")
 for k, v in sorted(rows.items(), key=lambda x: -x[1][1])[:25]:
     print(f"{k:72s} {v[0]:6d} {v[1] / 1e3:10.2f} {100 * v[1] / tot:6.1f}")
+# per-call durations (in launch order) of the fold chain and assign kernels
+pat = os.environ.get("KPROF_CALLS", "fold_|run_mark|run_emit|RadixSort|Select|filter_kernel|scan_kernel")
+import re  # noqa: E402
+seq = [(e.time_range.start if hasattr(e, "time_range") else 0, e.name[:40],
+        (e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total) / 1e3)
+       for e in prof.events() if e.device_type.name == "CUDA" and re.search(pat, e.name)]
+seq.sort()
+print("per-call ms (launch order):")
+line = []
+for _, nm, ms_ in seq:
+    line.append(f"{nm.split('(')[0].split('<')[0].replace('void ', '').replace('gp::', '')[-18:]}={ms_:.3f}")
+    if len(line) == 6:
+        print("  " + " ".join(line))
+        line = []
+if line:
+    print("  " + " ".join(line))
 print("device total ms", tot / 1e3, "rounds", sum(r.balance_rounds for r in stats.iterations),
       "iterations", len(stats.iterations))
 print("phase active rounds scanned/round evals/scanned")
@@ -48,7 +64,6 @@ for r in stats.iterations[::4] + stats.iterations[-3:]:
     print(r.phase, r.active_points, r.balance_rounds, sc // max(r.balance_rounds, 1),
           round(r.distance_evals / max(sc, 1), 2))
 
-os.environ["GP_BALANCE_GRAPH"] = "0"  # per-round timing needs the host-driven rounds
 t = _Timer()
 out, stats = partition_device(pts_d, w_d, s, device=dev, timer=t)
 torch.cuda.synchronize()
