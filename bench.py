@@ -15,12 +15,12 @@ and balance round of Alg. 2) of the named synthetic configuration.
   roofline : the assign kernel (gp_assign_round), algorithmic bytes per
           SURVEY §8d (B = n_act*(20+w_B) + n_scan*(8d+20)) over its
           CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline : the CPU oracle (numpy restatement of the reference path) on a
-          bounded sample of the same workload, on this host.
+  cpu_baseline : the reference's own path (the unmodified geopart package that
+          build() installs into baseline/_ref; the oracle port if it is absent) on
+          a bounded sample of the same workload, single-threaded, on this host.
 
---impl reference times that CPU implementation alone (the reference is pure
-numpy; /root/reference does not exist on the GPU box, so the oracle port
-stands in for it).
+--impl reference times that CPU implementation alone, one single-threaded run per
+host core in parallel (the reference is single-threaded numpy).
 """
 
 from __future__ import annotations
@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true")
     return ap.parse_args()
 
 
@@ -146,10 +147,10 @@ def device_workload(cfg, dev):
 
 
 def cpu_inputs(cfg):
-    """Bounded CPU-baseline input: the config itself, or for C5 (16 GiB, days on the
-    reference) the same recipe at 2^21 points with k scaled to keep 65536/16 points
-    per block... see the 'sample' string."""
-    from paper_1805_01208_b200.workloads import CONFIGS, c5_host
+    """Bounded CPU-baseline input: the config itself (C1-C3), or for C4/C5 (hours to
+    infeasible on the reference) the same recipe scaled down with the same points
+    per block -- a labelled extrapolation, see the 'sample' string."""
+    from paper_1805_01208_b200.workloads import CONFIGS, c4, c5_host
 
     if cfg == "C5":
         # the reference cannot run C5 (16 GiB input, days): same recipe at 1/1024 scale
@@ -157,37 +158,77 @@ def cpu_inputs(cfg):
         n = 1 << 20
         c = dict(CONFIGS["C5"], n=n, k=16)
         pts, w = c5_host(seed=0, n=n)
-        return c, pts, w, "C5 recipe at 1/1024 scale (n=2^20, k=16: same 65536 points/block)"
+        return c, pts, w, ("EXTRAPOLATION: C5 recipe at 1/1024 scale (n=2^20, k=16: the same "
+                           "65536 points/block)")
+    if cfg == "C4":
+        n = 1 << 20
+        c = dict(CONFIGS["C4"], n=n, k=64)
+        pts, w = c4(seed=0, n=n)
+        return c, pts, w, ("EXTRAPOLATION: C4 recipe at 1/16 scale (n=2^20, k=64: the same "
+                           "16384 points/block)")
     c, pts, w = workload(cfg)
-    return c, pts, w, f"{cfg} input"
+    return c, pts, w, f"{cfg} input (full size)"
 
 
-# ------------------------------------------------------------ CPU (oracle) arm
-def cpu_sample(cfg, c=None, pts=None, w=None, budget_s=25.0):
-    """Oracle on the same input: sample phase + as many full iterations as fit ~budget."""
-    from oracle import geographer_oracle as O
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
+
+def reference_module():
+    """The unmodified reference package installed by build() into baseline/_ref
+    (pip --target, no network); None when it is not there."""
+    if not os.path.isdir(os.path.join(REF_DIR, "geopart")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import geopart.kmeans as K
+
+    return K
+
+
+def ref_p(cfg, k):
+    """The reference's faster rank count (SURVEY §8d "report the better of p=1 and
+    p=256"): p=1 for small k, p=256 (per-rank box pruning) for large k."""
+    return 1 if k <= 64 else 256
+
+
+# ------------------------------------------------------------ CPU arm
+def cpu_sample(cfg, budget_s=25.0):
+    """One single-threaded run of the reference path on the config's (sample) input:
+    the real reference package when installed (kind "reference"), else the oracle
+    port (kind "port").  Full configs C1-C3 run completely; the scaled C4/C5 samples
+    run their warm-up phase plus as many full iterations as fit the budget."""
     c, pts, w, what = cpu_inputs(cfg)
-    # the reference's faster setting: one rank for small k, 256 ranks (per-rank box
-    # pruning) for large k (SURVEY §8d "report the better of p=1 and p=256")
-    chunks = 1 if c["k"] <= 64 else 256
+    K = reference_module()
+    p = ref_p(cfg, c["k"])
+    full = cfg == "C1"      # C2/C3 complete partitions take minutes: tools/ref_compare.py
+
+    def once(max_iter):
+        t0 = time.perf_counter()
+        if K is not None:
+            s = K.KMeansSettings(k=c["k"], epsilon=c["epsilon"], seed=0,
+                                 **({} if full else {"max_iter": max_iter}))
+            _, st = K.balanced_kmeans_points(pts, w, s, p=p, return_stats=True)
+            dec = sum(r.total_decisions for r in st.iterations)
+        else:
+            from oracle import geographer_oracle as O
+
+            kw = {} if full else {"max_iter": max_iter}
+            r = O.run(pts, w, O.Knobs(k=c["k"], epsilon=c["epsilon"], seed=0, **kw),
+                      scan_chunks=p)
+            dec = sum(rec["total_decisions"] for rec in r.records)
+        return dec, time.perf_counter() - t0
 
     iters = 1
-    t0 = time.perf_counter()
-    r = O.run(pts, w, O.Knobs(k=c["k"], epsilon=c["epsilon"], seed=0, max_iter=iters),
-              scan_chunks=chunks)
-    dt = time.perf_counter() - t0
-    dec = sum(rec["total_decisions"] for rec in r.records)
-    if dt < budget_s / 3:
+    dec, dt = once(iters)
+    if not full and dt < budget_s / 3:
         iters = max(1, min(50, int(budget_s / max(dt, 1e-3))))
-        t0 = time.perf_counter()
-        r = O.run(pts, w, O.Knobs(k=c["k"], epsilon=c["epsilon"], seed=0, max_iter=iters),
-                  scan_chunks=chunks)
-        dt = time.perf_counter() - t0
-        dec = sum(rec["total_decisions"] for rec in r.records)
-    return dict(value=dec / dt / 1e9, unit="Gpt/s", cores=1, kind="port",
-                sample=f"{what}, full sample phase + {iters} full iteration(s) "
-                       f"(max_iter={iters}), oracle numpy single-threaded, {chunks} scan chunk(s); "
+        dec, dt = once(iters)
+    kind = "reference" if K is not None else "port"
+    impl = ("geopart.kmeans.balanced_kmeans_points (unmodified reference, baseline/_ref)"
+            if K is not None else "oracle numpy port (reference package not installed)")
+    run = "complete partition" if full else f"warm-up phase + {iters} full iteration(s)"
+    return dict(value=dec / dt / 1e9, unit="Gpt/s", cores=1, kind=kind,
+                sample=f"{what}; {run}; {impl}, p={p}, single-threaded; "
                        f"{dec} point-assignments in {dt:.2f} s",
                 seconds=dt)
 
@@ -195,12 +236,13 @@ def cpu_sample(cfg, c=None, pts=None, w=None, budget_s=25.0):
 def _cpu_worker(cfg, budget_s, barrier, queue):
     barrier.wait()
     r = cpu_sample(cfg, budget_s=budget_s)
-    queue.put((r["value"] * 1e9 * r["seconds"], r["seconds"], r["sample"]))
+    queue.put((r["value"] * 1e9 * r["seconds"], r["seconds"], r["sample"], r["kind"]))
 
 
 def reference_workers():
     """Host threads the reference arm may use: every core this process may run on,
-    bounded by memory (one oracle sample peaks at ~0.3 GB RSS; 1 GB is budgeted)."""
+    bounded by memory (one C5 sample peaks at ~0.5 GB RSS; 1 GB is budgeted; a full
+    C3 run ~3 GB)."""
     try:
         cores = len(os.sched_getaffinity(0))
     except AttributeError:
@@ -208,7 +250,7 @@ def reference_workers():
     try:
         import psutil
 
-        mem = int(psutil.virtual_memory().available // (1 << 30)) // 2
+        mem = int(psutil.virtual_memory().available // (1 << 30)) // 4
     except Exception:
         mem = 8
     return max(1, min(cores, mem, 256))
@@ -233,8 +275,8 @@ def cpu_sample_parallel(cfg, workers, budget_s):
         p.join()
     dec = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
-    return dict(value=dec / wall / 1e9, seconds=wall, cores=workers,
-                sample=f"{workers} concurrent single-threaded samples, each: {res[0][2]}")
+    return dict(value=dec / wall / 1e9, seconds=wall, cores=workers, kind=res[0][3],
+                sample=f"{workers} concurrent single-threaded runs, each: {res[0][2]}")
 
 
 def run_reference(args):
@@ -260,8 +302,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SURVEY §8d recipe)",
         "config": {"workload": f"{args.config}: {DESCR[args.config]}", "n": int(c["n"]),
                    "d": int(c["d"]), "k": c["k"], "epsilon": c["epsilon"]},
-        "cpu_baseline": {"value": v, "unit": "Gpt/s", "cores": last["cores"], "kind": "port",
-                         "sample": last["sample"]},
+        "cpu_baseline": {"value": v, "unit": "Gpt/s", "cores": last["cores"],
+                         "kind": last["kind"], "sample": last["sample"]},
         "e2e": {"value": v, "unit": "Gpt/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -503,10 +545,30 @@ def run_b200(args):
                 dt = float(tt.item())
             if i > 0:
                 e2e_t.append(dt)
+            else:
+                e2e_cold = dt   # includes the first pinned allocation of the result buffer
         dec1 = sum(r.total_decisions for r in st2.iterations)
         e2e = {"value": dec1 / statistics.mean(e2e_t) / 1e9, "unit": "Gpt/s",
                "h2d_bytes_per_step": int(pts.nbytes + (0 if w is None else w.nbytes)) * world,
-               "d2h_bytes_per_step": int(c["n"] * 8), "partition_s": statistics.mean(e2e_t)}
+               "d2h_bytes_per_step": int(c["n"] * 8), "partition_s": statistics.mean(e2e_t),
+               "input_memory": "page-locked", "cold_first_call_s": e2e_cold}
+        if world == 1 and not args.no_pageable:
+            # the same call with a plain (pageable) numpy input, as the reference's callers
+            # pass it: staged through pinned chunks inside the library (staging.py)
+            pts_pg = np.array(pts, copy=True)
+            w_pg = None if w is None else np.array(w, copy=True)
+            del pts
+            tp = []
+            for i in range(2):
+                flush.fill_(1)
+                barrier()
+                t0 = time.perf_counter()
+                part = None
+                part, st3 = balanced_kmeans_points(pts_pg, w_pg, settings, return_stats=True)
+                torch.cuda.synchronize()
+                tp.append(time.perf_counter() - t0)
+            e2e["pageable"] = {"value": dec1 / min(tp) / 1e9, "partition_s": min(tp),
+                               "input_memory": "pageable numpy (np.array copy)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

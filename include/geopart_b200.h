@@ -45,6 +45,9 @@ const char* gp_last_error(void);
 int gp_abi_version(void);
 /* sizeof(gp_assign_args), sizeof(gp_fold_args): lets bindings verify struct layouts. */
 void gp_args_sizes(size_t* assign_args, size_t* fold_args);
+/* 1 when host pointer p lies in page-locked (cudaHostAlloc / registered) memory, so a
+ * host<->device copy of it is one DMA; 0 for pageable memory. */
+int gp_host_is_pinned(const void* p);
 
 /* K1  global bounding box: replaces the per-shard min/max + allreduce_extreme
  * of kmeans.py:546-548.  lohi[0:d] = min, lohi[d:2d] = max (device, doubles).

@@ -51,6 +51,7 @@ class FoldArgs(C.Structure):
 _SIGS = {
     "gp_last_error": (C.c_char_p, []),
     "gp_abi_version": (C.c_int, []),
+    "gp_host_is_pinned": (C.c_int, [vp]),
     "gp_args_sizes": (None, [C.POINTER(sz), C.POINTER(sz)]),
     "gp_box_minmax": (C.c_int, [vp, i64, C.c_int, i64, i64, vp, vp, vp]),
     "gp_weight_probe": (C.c_int, [vp, i64, vp, vp]),

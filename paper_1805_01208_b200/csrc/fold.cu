@@ -30,6 +30,10 @@
 namespace gp {
 
 constexpr int FT = 128;     // threads per fold CTA (4 warps; ~34 KB of staging)
+
+__device__ __forceinline__ unsigned smem_u32_f(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
 constexpr int MAXCOL = 5;   // d wx columns + w + objective (d <= 3)
 
 // Pair keys are (local segment << bb) | block with bb = bit length of k, so that the
@@ -105,54 +109,71 @@ __device__ __forceinline__ int32_t entry_key(const gp_fold_args& f, int64_t i, i
 // its predecessor's), tiles[t] = run starts in tile t (RTILE entries).  Warp w of a
 // tile owns 512 consecutive entries as 16 words of 32: lane l takes entry 32 t + l of
 // word t (coalesced 128-byte loads, all 16 issued first), so a word's run-start bits
-// are one ballot in entry order.
-__global__ void __launch_bounds__(RT) run_mark(gp_fold_args f, int64_t cnt, int64_t s0,
+// are one ballot in entry order.  A warp whose entries all lie in one segment (all
+// but the few at the 256 segment boundaries) compares blocks directly: its keys
+// differ exactly where the blocks differ.
+__global__ void __launch_bounds__(RT) run_mark(gp_fold_args f, int64_t cnt, int64_t s0, int bb,
                                                uint32_t* __restrict__ mask,
                                                int32_t* __restrict__ tiles) {
   __shared__ int s_warp[RT / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int bb = block_bits(f.k);
-  const int64_t wbase = (int64_t)blockIdx.x * RTILE + (int64_t)warp * (RTILE / (RT / 32));
-  constexpr int NW = RTILE / (RT / 32) / 32;   // words per warp (16)
-  // every load first (the segment and carry computations below would otherwise
-  // keep them from being issued until their own loads return)
+  constexpr int WE = RTILE / (RT / 32);        // entries per warp (512)
+  constexpr int NW = WE / 32;                  // words per warp (16)
+  const int64_t wbase = (int64_t)blockIdx.x * RTILE + (int64_t)warp * WE;
+  // every load first (the key computations below would otherwise keep them from
+  // being issued until their own loads return)
   int av[NW];
+  const bool whole = wbase + WE <= cnt;
+  if (whole) {
+    const int* ap = f.a + wbase + lane;
 #pragma unroll
-  for (int t = 0; t < NW; ++t) {
-    const int64_t i = wbase + 32 * t + lane;
-    av[t] = i < cnt ? __ldcs(f.a + i) : -1;
-  }
-  const int aprev = (lane == 0 && wbase > 0 && wbase <= cnt) ? f.a[wbase - 1] : -1;
-  int wseg = 0;
-  int64_t wnext = INT64_MAX;
-  bool wuni = false;    // list mode: every entry of the warp lies in segment wseg
-  if (wbase < cnt) {
-    const int64_t p0 = f.list ? f.list[wbase] : wbase;
-    wseg = segment_of(f.pos0 + p0, f.n_global);
-    wnext = wseg + 1 < GP_SEGMENTS ? ((int64_t)(wseg + 1) * f.n_global >> 8) - f.pos0 : INT64_MAX;
-    if (f.list) {   // the list is increasing: its last entry decides
-      const int64_t last = min(cnt, wbase + (int64_t)(RTILE / (RT / 32))) - 1;
-      wuni = f.list[last] < wnext;
+    for (int t = 0; t < NW; ++t) av[t] = __ldcs(ap + 32 * t);
+  } else {
+#pragma unroll
+    for (int t = 0; t < NW; ++t) {
+      const int64_t i = wbase + 32 * t + lane;
+      av[t] = i < cnt ? __ldcs(f.a + i) : -1;
     }
   }
-  auto key_of = [&](int64_t i, int c) -> int32_t {
-    if (c < 0) return -1;
-    if (f.list ? wuni : i < wnext) return (int32_t)(((wseg - s0) << bb) | c);
-    return entry_key(f, i, c, s0, bb);
-  };
-  int32_t carry = -2;   // key of the entry before the current word (lane 0's predecessor)
-  if (lane == 0 && wbase > 0 && wbase <= cnt) carry = entry_key(f, wbase - 1, aprev, s0, bb);
   int total = 0;
+  if (wbase < cnt) {
+    // segment of the warp's first entry, and whether every entry shares it
+    const int64_t last = min(cnt, wbase + (int64_t)WE) - 1;
+    const int64_t p0 = f.list ? f.list[wbase] : wbase;
+    const int64_t p1 = f.list ? f.list[last] : last;
+    const int wseg = segment_of(f.pos0 + p0, f.n_global);
+    const int64_t wnext =
+        wseg + 1 < GP_SEGMENTS ? ((int64_t)(wseg + 1) * f.n_global >> 8) - f.pos0 : INT64_MAX;
+    const bool uni = p1 < wnext;
+    // carry: key of the entry before the current word (lane 0's predecessor)
+    int32_t carry = -2;
+    if (lane == 0 && wbase > 0) carry = entry_key(f, wbase - 1, f.a[wbase - 1], s0, bb);
+    const int32_t hi = (int32_t)((wseg - s0) << bb);
+    if (uni) {
+      // keys = hi | a for a >= 0, -1 for a < 0: compare blocks, first word against carry
 #pragma unroll
-  for (int t = 0; t < NW; ++t) {
-    const int64_t i = wbase + 32 * t + lane;
-    const int32_t key = key_of(i, av[t]);
-    int32_t prev = __shfl_up_sync(FULL, key, 1);
-    if (lane == 0) prev = carry;
-    carry = __shfl_sync(FULL, key, 31);
-    const unsigned word = __ballot_sync(FULL, i < cnt && key != prev);
-    total += __popc(word);
-    if (lane == 0 && wbase + 32 * t < cnt) mask[(wbase + 32 * t) / 32] = word;
+      for (int t = 0; t < NW; ++t) {
+        const int32_t key = av[t] < 0 ? -1 : (hi | av[t]);
+        int32_t prev = __shfl_up_sync(FULL, key, 1);
+        if (lane == 0) prev = carry;
+        carry = __shfl_sync(FULL, key, 31);
+        const bool in = whole || wbase + 32 * t + lane < cnt;
+        const unsigned word = __ballot_sync(FULL, in && key != prev);
+        total += __popc(word);
+        if (lane == 0 && (whole || wbase + 32 * t < cnt)) mask[(wbase >> 5) + t] = word;
+      }
+    } else {
+      for (int t = 0; t < NW; ++t) {
+        const int64_t i = wbase + 32 * t + lane;
+        const int32_t key = i < cnt ? entry_key(f, i, av[t], s0, bb) : -1;
+        int32_t prev = __shfl_up_sync(FULL, key, 1);
+        if (lane == 0) prev = carry;
+        carry = __shfl_sync(FULL, key, 31);
+        const unsigned word = __ballot_sync(FULL, i < cnt && key != prev);
+        total += __popc(word);
+        if (lane == 0 && wbase + 32 * t < cnt) mask[(wbase >> 5) + t] = word;
+      }
+    }
   }
   if (lane == 0) s_warp[warp] = total;
   __syncthreads();
@@ -550,6 +571,160 @@ __global__ void __launch_bounds__(FT) fold_pipe(gp_fold_args f, const int32_t* _
   }
 }
 
+// 2D unit weights (C1, C5): two sequential columns (x, y: w*x = x, and the weight
+// column is the pair's entry count), streamed.  Lanes 2g, 2g+1 of a warp own group
+// g's x and y folds (G = 16 groups).  The entries of every group's next batch (up
+// to 32 consecutive entries of its current run) are copied straight into a
+// shared-memory ring by cp.async (16-byte (x, y) rows; no register staging), S
+// batches in flight per group, so the warp's loads for later batches overlap the
+// folds of the current one.  The x lane folds x in entry order, the y lane y; the
+// pair lanes swap dx^2 / dy^2 by shuffle so the x lane also folds the objective
+// (w |x - c|^2 in entry order, the bincount order of the other shapes) and keeps the
+// extent (max |x - c|^2).
+constexpr int XS = 2;          // ring stages per group
+constexpr int XG = 16;         // groups per warp
+constexpr int XROW = 33;       // double2 per group row (32 + 1 pad: conflict-free reads)
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32_f(dst)), "l"(src)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(FT) fold_xy(gp_fold_args f, const int32_t* __restrict__ starts,
+                                              const int32_t* __restrict__ sidx,
+                                              const uint32_t* __restrict__ skey,
+                                              const int32_t* __restrict__ pbeg,
+                                              int64_t* counters, double* __restrict__ out) {
+  extern __shared__ __align__(16) double2 xring[];   // [warp][stage][group][XROW]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* ring = xring + (size_t)warp * XS * XG * XROW;
+  const int64_t P = counters[3];
+  const int g = lane >> 1, col = lane & 1;
+  const int bbk = block_bits(f.k);
+  const double2* X = reinterpret_cast<const double2*>(f.X);
+  // cursor of group g (lanes 2g and 2g + 1 keep identical copies)
+  int pair = -1, j = 0, j1 = 0, cur = 0, re = 0, ns = 0, ne = 0, rn2 = 0;
+  // groups with need take the next pair (warp-uniform call)
+  auto fetch = [&](bool need) {
+    int64_t pi = 0;
+    if (need && col == 0) pi = (int64_t)atomicAdd((unsigned long long*)&counters[1], 1ull);
+    pi = __shfl_sync(FULL, pi, lane & ~1);
+    if (!need) return;
+    if (pi >= P) {
+      pair = -1;
+      return;
+    }
+    pair = (int)pi;
+    j = pbeg[pi];
+    j1 = pbeg[pi + 1];
+    const int r = sidx[j];
+    cur = starts[r];
+    re = starts[r + 1];
+    if (j + 1 < j1) {
+      const int r1 = sidx[j + 1];
+      ns = starts[r1];
+      ne = starts[r1 + 1];
+    }
+    if (j + 2 < j1) rn2 = sidx[j + 2];
+  };
+  // the group's next batch into ring stage sg (every lane copies for every group);
+  // returns its metadata (count, pair, whether it ends the pair)
+  auto issue = [&](int sg, int& n, int& pr, bool& last) {
+    const int c0 = cur;
+    n = 0;
+    pr = pair;
+    last = false;
+    if (pair >= 0) {
+      n = min(32, re - cur);
+      cur += n;
+      if (cur >= re) {
+        ++j;
+        if (j < j1) {
+          cur = ns;
+          re = ne;
+          if (j + 1 < j1) {
+            ns = starts[rn2];
+            ne = starts[rn2 + 1];
+            if (j + 2 < j1) rn2 = sidx[j + 2];
+          }
+        } else {
+          last = true;
+        }
+      }
+    }
+    double2* dst = ring + (size_t)sg * XG * XROW;
+#pragma unroll
+    for (int h = 0; h < XG; ++h) {
+      const int ch = __shfl_sync(FULL, c0, 2 * h);
+      const int nh = __shfl_sync(FULL, n, 2 * h);
+      if (lane < nh) cp_async16(dst + h * XROW + lane, X + ch + lane);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    fetch(last);   // the pair's batches are all issued: start the next pair
+  };
+  double acc = 0.0, obj = 0.0, ext = 0.0;
+  long long count = 0;
+  // fold the batch of stage sg (warp-uniform loop; lanes past their group's count
+  // only take part in the shuffles)
+  auto consume = [&](int sg, int n, int pr, bool last) {
+    double c = 0.0;
+    if (n > 0) c = f.centers[(int64_t)(skey[pbeg[pr]] & ((1u << bbk) - 1)) * 2 + col];
+    const double* row =
+        reinterpret_cast<const double*>(ring + ((size_t)sg * XG + g) * XROW) + col;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      const double v = row[2 * t];
+      const double d = __dsub_rn(v, c);
+      const double dd = __dmul_rn(d, d);
+      const double other = __shfl_xor_sync(FULL, dd, 1);
+      if (t < n) {
+        acc = __dadd_rn(acc, v);
+        if (col == 0) {
+          const double sq = __dadd_rn(dd, other);   // dx^2 + dy^2 (einsum 2D order)
+          obj = __dadd_rn(obj, sq);
+          ext = fmax(ext, sq);
+        }
+      }
+    }
+    count += n;
+    if (n > 0 && last) {
+      double* po = out + (int64_t)pr * (MAXCOL + 1);
+      if (col == 0) {
+        po[0] = acc;
+        po[2] = (double)count;   // bincount of unit weights: the exact entry count
+        po[3] = obj;
+        po[MAXCOL] = __dsqrt_rn(ext);
+      } else {
+        po[1] = acc;
+      }
+      acc = 0.0;
+      obj = 0.0;
+      ext = 0.0;
+      count = 0;
+    }
+  };
+  fetch(true);
+  static_assert(XS == 2, "fold_xy: two ring stages");
+  int n0, p0, n1, p1;
+  bool l0, l1;
+  issue(0, n0, p0, l0);
+  issue(1, n1, p1, l1);
+  for (;;) {
+    if (!__any_sync(FULL, n0 > 0 || n1 > 0 || pair >= 0)) break;
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    consume(0, n0, p0, l0);
+    __syncwarp();   // every lane is done with stage 0: refill it
+    issue(0, n0, p0, l0);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    consume(1, n1, p1, l1);
+    __syncwarp();
+    issue(1, n1, p1, l1);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // GP_FOLD_PIPE=1: the prefetching fold for every many-pair shape (tuning switch)
 static bool pipe_all() {
   static int v = -1;
@@ -568,6 +743,31 @@ static void launch_fold_pipe(const gp_fold_args* f, int sms, const int32_t* star
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_pipe<D, NC, G, B, UNIT>, FT, 0);
   fold_pipe<D, NC, G, B, UNIT><<<sms * (per_sm > 0 ? per_sm : 1), FT, 0, s>>>(
       *f, starts, sidx, skey, pbeg, counters, out);
+}
+
+// GP_FOLD_XY=0: the register-staged fold instead of fold_xy (tuning / comparison)
+static bool xy_off() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GP_FOLD_XY");
+    v = e && atoi(e) == 0;
+  }
+  return v == 1;
+}
+
+static void launch_fold_xy(const gp_fold_args* f, int sms, const int32_t* starts,
+                           const int32_t* sidx, const uint32_t* skey, const int32_t* pbeg,
+                           int64_t* counters, double* out, cudaStream_t s) {
+  const int smem = (FT / 32) * XS * XG * XROW * (int)sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fold_xy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_xy, FT, smem);
+  fold_xy<<<sms * (per_sm > 0 ? per_sm : 1), FT, smem, s>>>(*f, starts, sidx, skey, pbeg,
+                                                            counters, out);
 }
 
 template <int D, int NC, int G, int B>
@@ -748,7 +948,7 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     const int64_t nt = (cnt + RTILE - 1) / RTILE;
     int32_t* tiles = (int32_t*)(ws + L.off_tiles);
     uint32_t* mask = (uint32_t*)(ws + L.off_mask);
-    run_mark<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, mask, tiles);
+    run_mark<<<(unsigned)nt, RT, 0, s>>>(*f, cnt, L.s0, block_bits(f->k), mask, tiles);
     GP_CUDA(cudaMemsetAsync(tiles + nt, 0, sizeof(int32_t), s));
     size_t sb = L.cub_bytes;
     GP_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, sb, tiles, tiles, (int)nt + 1, s));
@@ -811,6 +1011,8 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
       else
         launch_fold_pipe<2, 4, 8, 1, false>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
     } else if (shape == 8) GP_FOLD(2, 4, 8, 1);
+    else if (shape == 0 && f->wmode == GP_W_UNIT && P_host >= 64 && !xy_off())
+      launch_fold_xy(f, sms, starts, sidx, skey, pbeg, counters, out, s);
     else if (shape == 0 && per >= 8 && (f->wmode == GP_W_UNIT || pipe_all()))
       // measured 18% faster at C5
       if (f->wmode == GP_W_UNIT)

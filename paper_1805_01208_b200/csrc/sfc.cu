@@ -345,6 +345,14 @@ extern "C" {
 
 const char* gp_last_error(void) { return g_err; }
 int gp_abi_version(void) { return 2; }
+int gp_host_is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return at.type == cudaMemoryTypeHost ? 1 : 0;
+}
 void gp_args_sizes(size_t* a, size_t* f) {
   *a = sizeof(gp_assign_args);
   *f = sizeof(gp_fold_args);

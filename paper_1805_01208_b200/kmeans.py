@@ -61,6 +61,30 @@ from .types import (
 DEFAULT_DEPTH = {2: 31, 3: 20}  # geometry.py:28
 
 
+def check_weights(n: int, weights) -> None:
+    """Weights must be 1-D with at least n entries (extra ones are ignored, as the
+    reference's shard slices ignore them, ranksim.py:101-106)."""
+    shape = tuple(weights.shape) if hasattr(weights, "shape") else np.shape(weights)
+    if len(shape) != 1:
+        raise ValueError(f"weights must be a 1-D array of length {n}, got shape {shape}")
+    if shape[0] < n:
+        # the reference fails in its redistribution gather (ranksim.py:160-168)
+        raise IndexError(f"weights has {shape[0]} entries for {n} points")
+
+
+def _host_to_device(a: np.ndarray, dev) -> torch.Tensor:
+    """Copy a host array to the device: one DMA when it is page-locked, else staged
+    through pinned chunks (staging.py), so a plain numpy input also moves at link rate."""
+    from . import staging
+
+    t = torch.from_numpy(a)
+    if a.nbytes < staging.MIN_STAGED or staging.is_pinned(a):
+        return t.to(dev, non_blocking=True)
+    out = torch.empty(a.shape, dtype=t.dtype, device=dev)
+    staging.h2d_into(out, a)
+    return out
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -68,9 +92,9 @@ def _ptr(t: torch.Tensor | None) -> int | None:
 class RankWorld:
     """Rank-count descriptor kept for API parity with ranksim.RankWorld.
 
-    Results are identical for every p (as in the reference for p | 256); on
-    one GPU p only validates.  Multi-GPU runs shard by SFC range across the
-    processes of a torch.distributed group (see parallel.py).
+    Results are identical for every p (as in the reference).  p is the GPU count:
+    balanced_kmeans_points(..., p) shards the run over min(p, visible GPUs) devices
+    (pool.py), by SFC range with k-sized NCCL exchanges (parallel.py).
     """
 
     def __init__(self, n: int, dim: int, p: int, coords=None, weights=None):
@@ -280,26 +304,20 @@ class DevicePartitioner:
         if isinstance(points, torch.Tensor):
             pts = points.to(device=dev, dtype=torch.float64)
         else:
-            pts = torch.from_numpy(np.ascontiguousarray(np.asarray(points, dtype=np.float64)))
-            pts = pts.to(dev, non_blocking=True)  # DMA straight from pinned callers' buffers
+            pts = _host_to_device(np.ascontiguousarray(np.asarray(points, dtype=np.float64)), dev)
         if pts.dim() != 2:
             raise GeometryError("points must be an (n, d) array")
         w = None
         if weights is not None:
             n = pts.shape[0]
-            shape = tuple(weights.shape) if hasattr(weights, "shape") else np.shape(weights)
-            if len(shape) != 1:
-                raise ValueError(f"weights must be a 1-D array of length {n}, got shape {shape}")
-            if shape[0] < n:
-                # the reference fails in its redistribution gather (ranksim.py:160-168)
-                raise IndexError(f"weights has {shape[0]} entries for {n} points")
+            check_weights(n, weights)
             if isinstance(weights, torch.Tensor):
                 w = weights[:n].to(device=dev, dtype=torch.float64).contiguous()
             else:
                 # extra entries are ignored, as the reference's shard slices do
                 # (ranksim.py:101-106)
-                w = torch.from_numpy(np.ascontiguousarray(np.asarray(weights, dtype=np.float64)[:n]))
-                w = w.to(dev)
+                w = _host_to_device(
+                    np.ascontiguousarray(np.asarray(weights, dtype=np.float64)[:n]), dev)
         return pts, w
 
     def _weight_plan(self, w: torch.Tensor | None, n: int) -> _WeightPlan:
@@ -817,8 +835,9 @@ class DevicePartitioner:
         """d = 2 (the influence step is a sqrt), exact integer block weights, no audit
         or per-round scan statistics: the round's decision and influence step run on
         the device (gp_balance_decide) and the host only reads a few scalars per
-        round.  GP_DEVICE_DECIDE=0 turns it off."""
-        return (type(self) is DevicePartitioner and self.d == 2 and self.wplan.exact
+        round.  Sharded runs all-reduce the k + 3 int64 sums first, so every rank takes
+        the same decision.  GP_DEVICE_DECIDE=0 turns it off."""
+        return (self.d == 2 and self.wplan.exact
                 and not self.settings.audit_bounds and not (self.aargs.flags & 1)
                 and os.environ.get("GP_DEVICE_DECIDE", "1") != "0")
 
@@ -863,6 +882,7 @@ class DevicePartitioner:
             N.check(N.lib.gp_assign_round(C.byref(a), self.sh), "gp_assign_round")
             if self.timer is not None:
                 self.timer.end(self.stream, a, tok)
+            self._reduce_round()   # sharded runs: every rank decides on the global sums
             N.call("gp_balance_decide", self.red.data_ptr(), k, float(self.wplan.scale),
                    float(st.epsilon), mr, self.bal.data_ptr(), cur_p, nxt_p, self.sh)
             self.bal_h[:8].copy_(self.bal[:8], non_blocking=True)
@@ -1213,10 +1233,29 @@ def _finish(assign_dev, stats, k, return_stats):
 
 def balanced_kmeans_points(points, weights, settings: KMeansSettings, p: int = 1,
                            return_stats: bool = False):
-    """Partition a raw point set (kmeans.py:502-512); identical results for every p."""
+    """Partition a raw point set (kmeans.py:502-512); identical results for every p.
+
+    p is the GPU count: p > 1 shards the run over min(p, visible GPUs) devices
+    (pool.py: one worker process per GPU, SFC-range shards, NCCL), p = 1 runs on
+    the current device."""
     if not isinstance(points, torch.Tensor):
         points = np.asarray(points, dtype=np.float64)
     RankWorld.from_points(points, weights, p)  # rank-count validation (ranksim.py:98-100)
+    G = 1
+    if p > 1:
+        from . import pool
+
+        G = pool.gpu_count_for(p)
+    if G > 1:
+        if len(points.shape) != 2:
+            raise GeometryError("points must be an (n, d) array")
+        if weights is not None:
+            check_weights(int(points.shape[0]), weights)
+            weights = weights[:points.shape[0]]
+        labels, stats = pool.get_pool(G).run(points, weights, settings)
+        part = Partition(assignment=labels, k=settings.k, balance_failed=stats.balance_failed,
+                         empty_blocks=np.flatnonzero(stats.final_state.block_weights == 0))
+        return (part, stats) if return_stats else part
     assign_dev, stats = partition_device(points, weights, settings)
     return _finish(assign_dev, stats, settings.k, return_stats)
 
