@@ -11,7 +11,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgeopart_b200.so")
+# GP_LIB_PATH: load a tuning variant built by `python -m paper_1805_01208_b200.build
+# --variant NAME -DX=Y` instead (experiments only)
+LIB_PATH = os.environ.get("GP_LIB_PATH") or os.path.join(_HERE, "libgeopart_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -135,7 +137,8 @@ KERNELS_PER_CALL = {
     "gp_box_minmax": 2, "gp_weight_probe": 1, "gp_hilbert_keys": 1, "gp_sort_pairs": 9,
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 4,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
-    "gp_scatter_by_gid": 1, "gp_gather_ranks": 1, "gp_group_boxes": 1,
+    "gp_scatter_by_gid": 1, "gp_gather_ranks": 1,
+    "gp_group_boxes": 1,
     "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 3, "gp_region_maps": 1, "gp_lb_remap": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
     "gp_sfc_cut": 3, "gp_predict": 1, "gp_balance_decide": 1, "gp_center_grid": 3,
 }

@@ -37,15 +37,18 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: list[str] | None = None) -> str:
+    lib = LIB if not variant else os.path.join(PKG, f"libgeopart_b200_{variant}.so")
+    if not variant and not force and up_to_date():
         return LIB
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build" if not variant else f"build_{variant}")
     os.makedirs(objdir, exist_ok=True)
     common = [NVCC, "-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
     if verbose:
         common += ["-Xptxas", "-v"]
+    common += list(defines or [])
     objs = []
     procs = []
     for src in sources():
@@ -59,12 +62,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(out.decode())
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     link = [NVCC, "-shared", *ARCH, "-o", tmp, *objs, "-lcudart"]
     subprocess.check_call(link)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else None
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=var, defines=defs))

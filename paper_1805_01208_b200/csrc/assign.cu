@@ -460,6 +460,9 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
 
 // -------------------------------------------------------------- scan kernel
 constexpr int STH = 256;           // 8 warps
+#ifndef GP_SCAN_OCC
+#define GP_SCAN_OCC 3              // resident scan CTAs per SM the register budget targets
+#endif
 constexpr int CAPW = 96;           // candidates staged per warp
 
 template <int D>
@@ -792,8 +795,47 @@ __global__ void __launch_bounds__(WKT) walk_kernel(gp_assign_args p, int wshift,
   tab_flush(tab, p.block_w, lane);
 }
 
+// near tie (or overflowed candidate set): the reference's exact arithmetic over every
+// candidate within the tolerance, (dist, index) tie-break.  Out of line: it is the
+// cold path, and keeping its IEEE div/sqrt sequences out of the scan loop keeps that
+// loop's code small (instruction-cache misses were a fifth of the scan's stalls).
+template <int D>
+__device__ __forceinline__ void exact_argmin(const gp_assign_args& p, WarpCand<D>& W,
+                                          const int32_t* src, int total, bool overflow,
+                                          bool valid, const double* x, double thr, int lane,
+                                          int& bi, float& bestf, float& secondf,
+                                          unsigned long long& nexact) {
+  double best = INFINITY, second = INFINITY;
+  int b = 0x7fffffff;
+  for (int c0 = 0; c0 < total; c0 += CAPW) {
+    const int cn = min(CAPW, total - c0);
+    if (overflow) {
+      __syncwarp();
+      for (int i = lane; i < cn; i += 32) stage<D>(W, i, src ? src[c0 + i] : c0 + i, p);
+      __syncwarp();
+    }
+    for (int i = 0; i < cn; ++i) {
+      if (valid && qdist<D>(x, W, i) <= thr) {
+        double cc[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) cc[j] = W.c[j][i];
+        const double dist = effdist_rn<D>(x, cc, W.inf[i], p.order3);
+        const int cid = W.cid[i];
+        const bool win = dist < best || (dist == best && cid < b);
+        second = win ? best : fmin(second, dist);
+        best = win ? dist : best;
+        b = win ? cid : b;
+        ++nexact;
+      }
+    }
+  }
+  bi = b;
+  bestf = __double2float_ru(best);
+  secondf = __double2float_rd(second);
+}
+
 template <int D, int WM>
-__global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
+__global__ void __launch_bounds__(STH, GP_SCAN_OCC) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
                                                    int sreg, const int32_t* __restrict__ scan,
                                                    const int32_t* __restrict__ olda,
                                                    const int32_t* __restrict__ runs,
@@ -1061,35 +1103,8 @@ __global__ void __launch_bounds__(STH, 3) scan_kernel(gp_assign_args p, int wshi
         bestf = __fmul_ru(__fsqrt_ru(__double2float_ru(q1)), AP_HI_F);
         secondf = i2 >= 0 ? __fmul_rd(__fsqrt_rd(__double2float_rd(q2)), AP_LO_F) : INFINITY;
       } else {
-        double best, second;
-        // near tie (or overflowed candidate set): the reference's exact arithmetic
-        best = INFINITY;
-        second = INFINITY;
-        bi = 0x7fffffff;
-        for (int c0 = 0; c0 < total; c0 += CAPW) {
-          const int cn = min(CAPW, total - c0);
-          if (overflow) {
-            __syncwarp();
-            for (int i = lane; i < cn; i += 32) stage<D>(W, i, src ? src[c0 + i] : c0 + i, p);
-            __syncwarp();
-          }
-          for (int i = 0; i < cn; ++i) {
-            if (valid && qdist<D>(x, W, i) <= thr) {
-              double cc[D];
-#pragma unroll
-              for (int j = 0; j < D; ++j) cc[j] = W.c[j][i];
-              const double dist = effdist_rn<D>(x, cc, W.inf[i], p.order3);
-              const int cid = W.cid[i];
-              const bool win = dist < best || (dist == best && cid < bi);
-              second = win ? best : fmin(second, dist);
-              best = win ? dist : best;
-              bi = win ? cid : bi;
-              ++nexact;
-            }
-          }
-        }
-        bestf = __double2float_ru(best);
-        secondf = __double2float_rd(second);
+        exact_argmin<D>(p, W, src, total, overflow, valid, x, thr, lane, bi, bestf, secondf,
+                        nexact);
       }
       // ---- write back + block weights of the scanned points
       RunW wv = 0;

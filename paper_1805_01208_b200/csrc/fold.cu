@@ -23,6 +23,7 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -31,9 +32,6 @@ namespace gp {
 
 constexpr int FT = 128;     // threads per fold CTA (4 warps; ~34 KB of staging)
 
-__device__ __forceinline__ unsigned smem_u32_f(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
 constexpr int MAXCOL = 5;   // d wx columns + w + objective (d <= 3)
 
 // Pair keys are (local segment << bb) | block with bb = bit length of k, so that the
@@ -571,160 +569,6 @@ __global__ void __launch_bounds__(FT) fold_pipe(gp_fold_args f, const int32_t* _
   }
 }
 
-// 2D unit weights (C1, C5): two sequential columns (x, y: w*x = x, and the weight
-// column is the pair's entry count), streamed.  Lanes 2g, 2g+1 of a warp own group
-// g's x and y folds (G = 16 groups).  The entries of every group's next batch (up
-// to 32 consecutive entries of its current run) are copied straight into a
-// shared-memory ring by cp.async (16-byte (x, y) rows; no register staging), S
-// batches in flight per group, so the warp's loads for later batches overlap the
-// folds of the current one.  The x lane folds x in entry order, the y lane y; the
-// pair lanes swap dx^2 / dy^2 by shuffle so the x lane also folds the objective
-// (w |x - c|^2 in entry order, the bincount order of the other shapes) and keeps the
-// extent (max |x - c|^2).
-constexpr int XS = 2;          // ring stages per group
-constexpr int XG = 16;         // groups per warp
-constexpr int XROW = 33;       // double2 per group row (32 + 1 pad: conflict-free reads)
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32_f(dst)), "l"(src)
-               : "memory");
-}
-
-__global__ void __launch_bounds__(FT) fold_xy(gp_fold_args f, const int32_t* __restrict__ starts,
-                                              const int32_t* __restrict__ sidx,
-                                              const uint32_t* __restrict__ skey,
-                                              const int32_t* __restrict__ pbeg,
-                                              int64_t* counters, double* __restrict__ out) {
-  extern __shared__ __align__(16) double2 xring[];   // [warp][stage][group][XROW]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double2* ring = xring + (size_t)warp * XS * XG * XROW;
-  const int64_t P = counters[3];
-  const int g = lane >> 1, col = lane & 1;
-  const int bbk = block_bits(f.k);
-  const double2* X = reinterpret_cast<const double2*>(f.X);
-  // cursor of group g (lanes 2g and 2g + 1 keep identical copies)
-  int pair = -1, j = 0, j1 = 0, cur = 0, re = 0, ns = 0, ne = 0, rn2 = 0;
-  // groups with need take the next pair (warp-uniform call)
-  auto fetch = [&](bool need) {
-    int64_t pi = 0;
-    if (need && col == 0) pi = (int64_t)atomicAdd((unsigned long long*)&counters[1], 1ull);
-    pi = __shfl_sync(FULL, pi, lane & ~1);
-    if (!need) return;
-    if (pi >= P) {
-      pair = -1;
-      return;
-    }
-    pair = (int)pi;
-    j = pbeg[pi];
-    j1 = pbeg[pi + 1];
-    const int r = sidx[j];
-    cur = starts[r];
-    re = starts[r + 1];
-    if (j + 1 < j1) {
-      const int r1 = sidx[j + 1];
-      ns = starts[r1];
-      ne = starts[r1 + 1];
-    }
-    if (j + 2 < j1) rn2 = sidx[j + 2];
-  };
-  // the group's next batch into ring stage sg (every lane copies for every group);
-  // returns its metadata (count, pair, whether it ends the pair)
-  auto issue = [&](int sg, int& n, int& pr, bool& last) {
-    const int c0 = cur;
-    n = 0;
-    pr = pair;
-    last = false;
-    if (pair >= 0) {
-      n = min(32, re - cur);
-      cur += n;
-      if (cur >= re) {
-        ++j;
-        if (j < j1) {
-          cur = ns;
-          re = ne;
-          if (j + 1 < j1) {
-            ns = starts[rn2];
-            ne = starts[rn2 + 1];
-            if (j + 2 < j1) rn2 = sidx[j + 2];
-          }
-        } else {
-          last = true;
-        }
-      }
-    }
-    double2* dst = ring + (size_t)sg * XG * XROW;
-#pragma unroll
-    for (int h = 0; h < XG; ++h) {
-      const int ch = __shfl_sync(FULL, c0, 2 * h);
-      const int nh = __shfl_sync(FULL, n, 2 * h);
-      if (lane < nh) cp_async16(dst + h * XROW + lane, X + ch + lane);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    fetch(last);   // the pair's batches are all issued: start the next pair
-  };
-  double acc = 0.0, obj = 0.0, ext = 0.0;
-  long long count = 0;
-  // fold the batch of stage sg (warp-uniform loop; lanes past their group's count
-  // only take part in the shuffles)
-  auto consume = [&](int sg, int n, int pr, bool last) {
-    double c = 0.0;
-    if (n > 0) c = f.centers[(int64_t)(skey[pbeg[pr]] & ((1u << bbk) - 1)) * 2 + col];
-    const double* row =
-        reinterpret_cast<const double*>(ring + ((size_t)sg * XG + g) * XROW) + col;
-#pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      const double v = row[2 * t];
-      const double d = __dsub_rn(v, c);
-      const double dd = __dmul_rn(d, d);
-      const double other = __shfl_xor_sync(FULL, dd, 1);
-      if (t < n) {
-        acc = __dadd_rn(acc, v);
-        if (col == 0) {
-          const double sq = __dadd_rn(dd, other);   // dx^2 + dy^2 (einsum 2D order)
-          obj = __dadd_rn(obj, sq);
-          ext = fmax(ext, sq);
-        }
-      }
-    }
-    count += n;
-    if (n > 0 && last) {
-      double* po = out + (int64_t)pr * (MAXCOL + 1);
-      if (col == 0) {
-        po[0] = acc;
-        po[2] = (double)count;   // bincount of unit weights: the exact entry count
-        po[3] = obj;
-        po[MAXCOL] = __dsqrt_rn(ext);
-      } else {
-        po[1] = acc;
-      }
-      acc = 0.0;
-      obj = 0.0;
-      ext = 0.0;
-      count = 0;
-    }
-  };
-  fetch(true);
-  static_assert(XS == 2, "fold_xy: two ring stages");
-  int n0, p0, n1, p1;
-  bool l0, l1;
-  issue(0, n0, p0, l0);
-  issue(1, n1, p1, l1);
-  for (;;) {
-    if (!__any_sync(FULL, n0 > 0 || n1 > 0 || pair >= 0)) break;
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    __syncwarp();
-    consume(0, n0, p0, l0);
-    __syncwarp();   // every lane is done with stage 0: refill it
-    issue(0, n0, p0, l0);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    __syncwarp();
-    consume(1, n1, p1, l1);
-    __syncwarp();
-    issue(1, n1, p1, l1);
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
 // GP_FOLD_PIPE=1: the prefetching fold for every many-pair shape (tuning switch)
 static bool pipe_all() {
   static int v = -1;
@@ -743,31 +587,6 @@ static void launch_fold_pipe(const gp_fold_args* f, int sms, const int32_t* star
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_pipe<D, NC, G, B, UNIT>, FT, 0);
   fold_pipe<D, NC, G, B, UNIT><<<sms * (per_sm > 0 ? per_sm : 1), FT, 0, s>>>(
       *f, starts, sidx, skey, pbeg, counters, out);
-}
-
-// GP_FOLD_XY=0: the register-staged fold instead of fold_xy (tuning / comparison)
-static bool xy_off() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GP_FOLD_XY");
-    v = e && atoi(e) == 0;
-  }
-  return v == 1;
-}
-
-static void launch_fold_xy(const gp_fold_args* f, int sms, const int32_t* starts,
-                           const int32_t* sidx, const uint32_t* skey, const int32_t* pbeg,
-                           int64_t* counters, double* out, cudaStream_t s) {
-  const int smem = (FT / 32) * XS * XG * XROW * (int)sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fold_xy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fold_xy, FT, smem);
-  fold_xy<<<sms * (per_sm > 0 ? per_sm : 1), FT, smem, s>>>(*f, starts, sidx, skey, pbeg,
-                                                            counters, out);
 }
 
 template <int D, int NC, int G, int B>
@@ -1011,8 +830,6 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
       else
         launch_fold_pipe<2, 4, 8, 1, false>(f, sms, starts, sidx, skey, pbeg, counters, out, s);
     } else if (shape == 8) GP_FOLD(2, 4, 8, 1);
-    else if (shape == 0 && f->wmode == GP_W_UNIT && P_host >= 64 && !xy_off())
-      launch_fold_xy(f, sms, starts, sidx, skey, pbeg, counters, out, s);
     else if (shape == 0 && per >= 8 && (f->wmode == GP_W_UNIT || pipe_all()))
       // measured 18% faster at C5
       if (f->wmode == GP_W_UNIT)

@@ -85,6 +85,17 @@ def _host_to_device(a: np.ndarray, dev) -> torch.Tensor:
     return out
 
 
+# GP_NVTX=1: every assign round inside an NVTX range "round<N>" (N counts the rounds of
+# the process), so an ncu capture can select one round (--nvtx --nvtx-include round550/)
+_NVTX = os.environ.get("GP_NVTX") == "1"
+_ROUNDS = [0]
+
+
+def _round_counter() -> int:
+    _ROUNDS[0] += 1
+    return _ROUNDS[0] - 1
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -677,8 +688,12 @@ class DevicePartitioner:
         self.red.zero_()
         if self.timer is not None:
             tok = self.timer.begin(self.stream, self.aargs)
+        if _NVTX:
+            torch.cuda.nvtx.range_push(f"round{_round_counter()}")
         N.count("gp_assign_round")
         N.check(N.lib.gp_assign_round(C.byref(self.aargs), self.sh), "gp_assign_round")
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
         if self.timer is not None:
             self.timer.end(self.stream, self.aargs, tok)
         self._reduce_round()
@@ -878,8 +893,12 @@ class DevicePartitioner:
             self.red.zero_()
             if self.timer is not None:
                 tok = self.timer.begin(self.stream, a)
+            if _NVTX:
+                torch.cuda.nvtx.range_push(f"round{_round_counter()}")
             N.count("gp_assign_round")
             N.check(N.lib.gp_assign_round(C.byref(a), self.sh), "gp_assign_round")
+            if _NVTX:
+                torch.cuda.nvtx.range_pop()
             if self.timer is not None:
                 self.timer.end(self.stream, a, tok)
             self._reduce_round()   # sharded runs: every rank decides on the global sums
