@@ -64,6 +64,11 @@ int gp_weight_probe(const double* w, int64_t n, int64_t* out, void* stream);
 /* K2  Hilbert keys: replaces geometry.py:112-132 (point_cells) +
  * geometry.py:135-179 (hilbert_cell_keys) + geometry.py:182-192.  Bit-exact.
  * gids (nullable) receives gid_base + i. */
+/* Host-only check of the table form of the key (gp_hilbert_keys runs the transpose
+ * as a finite-state machine, several levels per lookup): rebuilds the tables for
+ * dimension d and compares them with gp_hilbert_cell_key_host on random cells at every
+ * depth.  0 = they agree. */
+int gp_hilbert_fsm_selfcheck(int d);
 int gp_hilbert_keys(const double* pts, int64_t n, int d, int64_t stride_pt, int64_t stride_dim,
                     const double* lohi, int depth, uint64_t* keys, uint32_t* gids,
                     uint32_t gid_base, void* stream);

@@ -59,6 +59,7 @@ _SIGS = {
     "gp_weight_probe": (C.c_int, [vp, i64, vp, vp]),
     "gp_hilbert_keys": (C.c_int, [vp, i64, C.c_int, i64, i64, vp, C.c_int, vp, vp, u32, vp]),
     "gp_hilbert_cell_key_host": (u64, [C.POINTER(u32), C.c_int, C.c_int]),
+    "gp_hilbert_fsm_selfcheck": (C.c_int, [C.c_int]),
     "gp_sort_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_sort_pairs": (C.c_int, [vp, vp, vp, vp, i64, C.c_int, vp, sz, vp]),
     "gp_gather_points": (C.c_int, [vp, i64, i64, C.c_int, vp, i64, vp, i64, vp, C.c_int, vp,

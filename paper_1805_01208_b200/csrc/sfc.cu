@@ -10,6 +10,9 @@
 
 #include <cub/device/device_scan.cuh>
 
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 namespace gp {
@@ -154,11 +157,114 @@ __device__ __forceinline__ uint64_t interleave(const uint32_t* X) {
   return (spread3(X[0]) << 2) | (spread3(X[1]) << 1) | spread3(X[2]);
 }
 
+// The transpose above as a finite-state machine over levels, top level first (the
+// form the kernel runs).  Processing level b with the cells' raw bits r:
+//   t = g(r)                  bits as transformed by the operations of the levels above;
+//   G = gray(t)               G_0 = t_0, G_i = t_i ^ G_{i-1}       (the Gray loop);
+//   F = G ^ par               par = xor of G_{d-1} over the levels above (the t loop);
+//   key <- key . F_0 .. F_{d-1}                                     (the interleave);
+//   g <- h(t) o g             h: for i = 0..d-1, invert axis 0 if t_i, else swap
+//                             axes 0 and i (the operations on the lower bits);
+//   par <- par ^ G_{d-1}.
+// g ranges over a few signed axis permutations, so (g, par) is a small state and L
+// levels at a time become one table lookup: entry [state][d*L raw bits] = the d*L key
+// bits | next state << (d*L).  The tables are built on the host from this definition
+// (hilbert_fsm_tables) and checked against the transpose at load (gp_hilbert_keys).
+struct HFsm {
+  int states;
+  int L;                           // levels per multi-level lookup
+  uint16_t multi[96 * 256];        // [state][raw chunk]
+  uint16_t single[96 * 8];         // [state][raw level]
+};
+__device__ HFsm g_hfsm[2];         // d = 2, d = 3
+
+static void hilbert_fsm_tables(int d, HFsm& T) {
+  const int nv = 1 << d;
+  std::vector<std::vector<int>> gs;   // reachable transforms (maps on d-bit vectors)
+  std::vector<int> ident(nv);
+  for (int v = 0; v < nv; ++v) ident[v] = v;
+  gs.push_back(ident);
+  auto level_op = [&](int t) {
+    std::vector<int> h(nv);
+    for (int v = 0; v < nv; ++v) {
+      int bits[3] = {v & 1, (v >> 1) & 1, (v >> 2) & 1};
+      for (int i = 0; i < d; ++i) {
+        if ((t >> i) & 1) bits[0] ^= 1;
+        else std::swap(bits[0], bits[i]);
+      }
+      h[v] = bits[0] | (bits[1] << 1) | (bits[2] << 2);
+    }
+    return h;
+  };
+  auto index_of = [&](const std::vector<int>& g) {
+    for (size_t k = 0; k < gs.size(); ++k)
+      if (gs[k] == g) return (int)k;
+    gs.push_back(g);
+    return (int)gs.size() - 1;
+  };
+  // one level from (g index, par) with raw bits r: out F bits (axis 0 most significant),
+  // next (g index, par)
+  auto step = [&](int gi, int par, int r, int& F, int& ngi, int& npar) {
+    const std::vector<int> g = gs[gi];
+    const int t = g[r];
+    int G[3], prev = 0;
+    for (int i = 0; i < d; ++i) {
+      G[i] = ((t >> i) & 1) ^ (i ? prev : 0);
+      prev = G[i];
+    }
+    F = 0;
+    for (int i = 0; i < d; ++i) F = (F << 1) | (G[i] ^ par);
+    const std::vector<int> h = level_op(t);
+    std::vector<int> ng(nv);
+    for (int v = 0; v < nv; ++v) ng[v] = h[g[v]];
+    ngi = index_of(ng);
+    npar = par ^ G[d - 1];
+  };
+  for (size_t gi = 0; gi < gs.size(); ++gi)      // close the state set
+    for (int r = 0; r < nv; ++r) {
+      int F, ngi, np;
+      step((int)gi, 0, r, F, ngi, np);
+    }
+  T.states = 2 * (int)gs.size();
+  T.L = d == 2 ? 4 : 2;
+  const int L = T.L, nin = 1 << (d * L);
+  for (int st = 0; st < T.states; ++st) {
+    for (int r = 0; r < nv; ++r) {
+      int F, ngi, np;
+      step(st >> 1, st & 1, r, F, ngi, np);
+      T.single[st * 8 + r] = (uint16_t)(F | ((2 * ngi + np) << d));
+    }
+    for (int c = 0; c < nin; ++c) {
+      int gi = st >> 1, par = st & 1, key = 0;
+      for (int l = 0; l < L; ++l) {   // top level of the chunk first
+        int r = 0;
+        for (int i = 0; i < d; ++i) r |= ((c >> (i * L + (L - 1 - l))) & 1) << i;
+        int F, ngi, np;
+        step(gi, par, r, F, ngi, np);
+        key = (key << d) | F;
+        gi = ngi;
+        par = np;
+      }
+      T.multi[st * 256 + c] = (uint16_t)(key | ((2 * gi + par) << (d * L)));
+    }
+  }
+}
+
 template <int D>
 __global__ void hilbert_kernel(const double* __restrict__ pts, int64_t n, int64_t sp, int64_t sd,
                                const double* __restrict__ lohi, int depth,
                                uint64_t* __restrict__ keys, uint32_t* __restrict__ gids,
                                uint32_t gid_base) {
+  __shared__ uint16_t s_multi[96 * 64 > 16 * 256 ? 96 * 64 : 16 * 256];
+  __shared__ uint16_t s_single[96 * 8];
+  const HFsm& T = g_hfsm[D - 2];
+  constexpr int L = D == 2 ? 4 : 2;
+  constexpr int NIN = 1 << (D * L);
+  const int S = T.states;
+  for (int e = threadIdx.x; e < S * NIN; e += blockDim.x)
+    s_multi[e] = T.multi[(e / NIN) * 256 + (e % NIN)];
+  for (int e = threadIdx.x; e < S * 8; e += blockDim.x) s_single[e] = T.single[e];
+  __syncthreads();
   double lo[D], safe[D];
   const double side = (double)(1ull << depth);
   const double top = side - 1.0;
@@ -178,8 +284,27 @@ __global__ void hilbert_kernel(const double* __restrict__ pts, int64_t n, int64_
       double c = fmin(fmax(floor(s), 0.0), top);
       X[j] = (uint32_t)c;
     }
-    hilbert_transpose<D>(X, depth);
-    keys[i] = interleave<D>(X);
+    // the transpose + interleave as table steps, top level first
+    uint64_t key = 0;
+    int st = 0;
+    int b = depth - 1;                     // next level to consume
+    for (; b + 1 >= L; b -= L) {
+      int c = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) c |= (int)((X[j] >> (b + 1 - L)) & ((1u << L) - 1)) << (j * L);
+      const unsigned e = s_multi[st * NIN + c];
+      key = (key << (D * L)) | (e & ((1u << (D * L)) - 1));
+      st = (int)(e >> (D * L));
+    }
+    for (; b >= 0; --b) {
+      int r = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) r |= (int)((X[j] >> b) & 1u) << j;
+      const unsigned e = s_single[st * 8 + r];
+      key = (key << D) | (e & ((1u << D) - 1));
+      st = (int)(e >> D);
+    }
+    keys[i] = key;
     if (gids) gids[i] = gid_base + (uint32_t)i;
   }
 }
@@ -381,6 +506,53 @@ int gp_weight_probe(const double* w, int64_t n, int64_t* out, void* stream) {
   return check_launch("weight_probe");
 }
 
+// build the tables for dimension d and check them against the transpose on random
+// cells at every depth (host only)
+static uint64_t fsm_key(const HFsm& T, int d, int depth, const uint32_t* X) {
+  uint64_t key = 0;
+  int st = 0, b = depth - 1;
+  const int L = T.L;
+  for (; b + 1 >= L; b -= L) {
+    int ch = 0;
+    for (int j = 0; j < d; ++j) ch |= (int)((X[j] >> (b + 1 - L)) & ((1u << L) - 1)) << (j * L);
+    const unsigned e = T.multi[st * 256 + ch];
+    key = (key << (d * L)) | (e & ((1u << (d * L)) - 1));
+    st = (int)(e >> (d * L));
+  }
+  for (; b >= 0; --b) {
+    int r = 0;
+    for (int j = 0; j < d; ++j) r |= (int)((X[j] >> b) & 1u) << j;
+    const unsigned e = T.single[st * 8 + r];
+    key = (key << d) | (e & ((1u << d) - 1));
+    st = (int)(e >> d);
+  }
+  return key;
+}
+
+static int hilbert_fsm_checked(int d, HFsm& T) {
+  hilbert_fsm_tables(d, T);
+  GP_REQUIRE(T.states <= (d == 2 ? 16 : 96), "hilbert tables: unexpected state count");
+  uint64_t rs = 0x243F6A8885A308D3ull;
+  for (int dep = 1; d * dep <= 62; ++dep)
+    for (int trial = 0; trial < 512; ++trial) {
+      uint32_t c[3];
+      for (int j = 0; j < d; ++j) {
+        rs = rs * 6364136223846793005ull + 1442695040888963407ull;
+        c[j] = (uint32_t)(rs >> 33) & (uint32_t)((1ull << dep) - 1);
+      }
+      const uint64_t want = gp_hilbert_cell_key_host(c, d, dep);
+      GP_REQUIRE(fsm_key(T, d, dep, c) == want,
+                 "hilbert tables disagree with the transpose (d=%d depth=%d)", d, dep);
+    }
+  return GP_OK;
+}
+
+int gp_hilbert_fsm_selfcheck(int d) {
+  GP_REQUIRE(d == 2 || d == 3, "gp_hilbert_fsm_selfcheck: d must be 2 or 3");
+  static HFsm T;
+  return hilbert_fsm_checked(d, T);
+}
+
 int gp_hilbert_keys(const double* pts, int64_t n, int d, int64_t stride_pt, int64_t stride_dim,
                     const double* lohi, int depth, uint64_t* keys, uint32_t* gids,
                     uint32_t gid_base, void* stream) {
@@ -388,6 +560,16 @@ int gp_hilbert_keys(const double* pts, int64_t n, int d, int64_t stride_pt, int6
   GP_REQUIRE(depth >= 1 && d * depth <= 62, "gp_hilbert_keys: depth %d out of range for d=%d",
              depth, d);
   if (n == 0) return GP_OK;
+  static bool tables = false;
+  if (!tables) {
+    for (int dd = 2; dd <= 3; ++dd) {
+      static HFsm T;
+      int rc = hilbert_fsm_checked(dd, T);
+      if (rc) return rc;
+      GP_CUDA(cudaMemcpyToSymbol(g_hfsm, &T, sizeof(HFsm), (dd - 2) * sizeof(HFsm)));
+    }
+    tables = true;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   if (d == 2)
     hilbert_kernel<2><<<stride_grid(n), 256, 0, s>>>(pts, n, stride_pt, stride_dim, lohi, depth,

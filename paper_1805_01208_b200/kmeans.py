@@ -96,6 +96,14 @@ def _round_counter() -> int:
     return _ROUNDS[0] - 1
 
 
+_FOLDS = [0]
+
+
+def _fold_counter() -> int:
+    _FOLDS[0] += 1
+    return _FOLDS[0] - 1
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -346,6 +354,15 @@ class DevicePartitioner:
         return _WeightPlan(mode, bool(exact), 2.0 ** s if exact else 1.0)
 
     def bootstrap(self, points, weights):
+        if _NVTX:
+            torch.cuda.nvtx.range_push("bootstrap")
+        try:
+            return self._bootstrap(points, weights)
+        finally:
+            if _NVTX:
+                torch.cuda.nvtx.range_pop()
+
+    def _bootstrap(self, points, weights):
         st = self.settings
         pts, w = self._input(points, weights)
         n, d = pts.shape
@@ -732,8 +749,12 @@ class DevicePartitioner:
         else:
             f.X, f.a, f.w = self.X.data_ptr(), self.A.data_ptr(), _ptr(self.W)
             f.list, f.m = None, 0
+        if _NVTX:
+            torch.cuda.nvtx.range_push(f"fold{_fold_counter()}")
         N.count("gp_movement_fold")
         N.check(N.lib.gp_movement_fold(C.byref(f), self.sh), "gp_movement_fold")
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
 
     def _block_weights(self, blk_int):
         if self.wplan.exact:
@@ -984,6 +1005,15 @@ class DevicePartitioner:
 
     def _deliver(self, A):
         """int64 assignment by original id (kmeans.py:637-641)."""
+        if _NVTX:
+            torch.cuda.nvtx.range_push("deliver")
+        try:
+            return self._deliver_ids(A)
+        finally:
+            if _NVTX:
+                torch.cuda.nvtx.range_pop()
+
+    def _deliver_ids(self, A):
         out = torch.empty(self.n, dtype=torch.int64, device=self.device)
         N.call("gp_scatter_by_gid", A.data_ptr(), self.gids.data_ptr(), self.n, out.data_ptr(),
                self.sh)

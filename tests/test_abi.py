@@ -77,3 +77,10 @@ def test_errors_are_reported_not_raised(native):
     assert b"unsupported dimension" in native.lib.gp_last_error()
     rc = native.lib.gp_hilbert_keys(None, 10, 3, 3, 1, None, 21, None, None, 0, None)
     assert rc == 1 and b"depth" in native.lib.gp_last_error()
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_hilbert_fsm_tables_match_transpose(native, d):
+    """The kernel's table form of the key (several levels per lookup) agrees with the
+    transpose of geometry.py:135-179 at every depth (host-only check)."""
+    assert native.lib.gp_hilbert_fsm_selfcheck(d) == 0, native.lib.gp_last_error()
