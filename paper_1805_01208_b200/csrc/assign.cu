@@ -85,15 +85,12 @@ __device__ __forceinline__ double box_lsq(const double* c, const double* lo, con
 }
 
 // fresh best / runner-up effective distances (b rounded up, s rounded down)
-// -> normalised float32 bounds under the current maps.  A negative ub~ (the point
-// sits closer to its center than the accumulated shift T) is stored as 0: S*0 + T is
-// still an upper bound (S > 0), and every stored ub~ >= 0 lets the filter evaluate
-// ub = fmaf_ru(S, ub~, T) without the sign select.
+// -> normalised float32 bounds under the current maps
 __device__ __forceinline__ void store_bounds(const gp_assign_args& p, const float4& L, int64_t q,
                                              int c, float b_up, float s_dn) {
   const float4 N = reinterpret_cast<const float4*>(p.ub_norm)[c];
   reinterpret_cast<unsigned*>(p.ublb)[q] =
-      bnd_pack(fmaxf(ub_normf(N, b_up), 0.f), lb_normf(L.z, L.w, s_dn), p.bound_scale);
+      bnd_pack(ub_normf(N, b_up), lb_normf(L.z, L.w, s_dn), p.bound_scale);
 }
 
 // lower bound of min_c 1/infl_c^2: the device copy gp_update_maps keeps (so that a
@@ -355,7 +352,7 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
           // without its floor at 0: the evaluated ub is a sound upper bound of a
           // distance, so it is >= 0 and "ub < lb" is unchanged by the floor
           const float lbv = __fmaf_rd(lbp.x, lb[e], -lbp.y);
-          keep |= (unsigned)(__fmaf_ru(E.x, ub[e], E.z) < lbv) << e;   // stored ub~ >= 0
+          keep |= (unsigned)(ub_evalf(E, ub[e]) < lbv) << e;
         }
         need = keep ^ ((1u << FPER) - 1);
         if (keep) {
