@@ -179,6 +179,22 @@ class _Timer:
         return f, s
 
 
+def sort_pairs(keys: torch.Tensor, vals: torch.Tensor | None, keys_out: torch.Tensor | None,
+               vals_out: torch.Tensor, key_bits: int, stream) -> None:
+    """(key, val) pairs in stable key order (np.lexsort((gids, keys)), ranksim.py:158,
+    when vals are the input positions): the onesweep device radix sort, gp_sort_pairs.
+    vals None means val = input index."""
+    n = keys.shape[0]
+    dev = keys.device
+    if vals is None:
+        vals = torch.arange(n, dtype=torch.int32, device=dev)
+    ko = keys_out if keys_out is not None else torch.empty_like(keys)
+    wsb = N.size_query("gp_sort_workspace_bytes", n)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    N.call("gp_sort_pairs", keys.data_ptr(), vals.data_ptr(), ko.data_ptr(), vals_out.data_ptr(),
+           n, key_bits, ws.data_ptr(), wsb, stream)
+
+
 def sample_ranks_device(n: int, seed: int, device, stream) -> torch.Tensor:
     """Inverse of numpy.random.default_rng(seed).permutation(n), computed on the GPU.
 
@@ -390,17 +406,14 @@ class DevicePartitioner:
         self.wplan = self._weight_plan(w, n)
         # K2 keys + K3 sort + payload gather (geometry.py:182, ranksim.py:143-170)
         keys = torch.empty(n, dtype=torch.int64, device=dev)
-        gids = torch.empty(n, dtype=torch.int32, device=dev)
         N.call("gp_hilbert_keys", pts.data_ptr(), n, d, sp, sd, lohi.data_ptr(), depth,
-               keys.data_ptr(), gids.data_ptr(), 0, sh)
-        keys_s = torch.empty_like(keys)
-        self.gids = torch.empty_like(gids)
-        wsb = N.size_query("gp_sort_workspace_bytes", n)
-        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
-        N.call("gp_sort_pairs", keys.data_ptr(), gids.data_ptr(), keys_s.data_ptr(),
-               self.gids.data_ptr(), n, d * depth, ws.data_ptr(), wsb, sh)
-        self.keys_sorted = keys_s if self.keep_keys else None
-        del keys, gids, ws, keys_s
+               keys.data_ptr(), None, 0, sh)
+        # gids are the input positions (ranksim.py:98-107): the sort's implicit vals
+        self.gids = torch.empty(n, dtype=torch.int32, device=dev)
+        keys_s = torch.empty_like(keys) if self.keep_keys else None
+        sort_pairs(keys, None, keys_s, self.gids, d * depth, sh)
+        self.keys_sorted = keys_s
+        del keys, keys_s
         self.ldx = d
         self.X = torch.empty((n, d), dtype=torch.float64, device=dev)  # AoS, SFC order
         self.W = None
@@ -1046,15 +1059,10 @@ class DistributedPartitioner(DevicePartitioner):
 
     # ---------------------------------------------------------------- bootstrap
     def _device_sort(self, keys: torch.Tensor) -> torch.Tensor:
-        """Stable permutation sorting int64 keys (device radix sort, gp_sort_pairs)."""
+        """Stable permutation sorting int64 keys (device radix sort, sort_pairs)."""
         m = keys.shape[0]
-        vals = torch.arange(m, dtype=torch.int32, device=keys.device)
-        ko = torch.empty_like(keys)
-        vo = torch.empty_like(vals)
-        wsb = N.size_query("gp_sort_workspace_bytes", m)
-        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=keys.device)
-        N.call("gp_sort_pairs", keys.data_ptr(), vals.data_ptr(), ko.data_ptr(), vo.data_ptr(), m,
-               self.key_bits, ws.data_ptr(), wsb, self.sh)
+        vo = torch.empty(m, dtype=torch.int32, device=keys.device)
+        sort_pairs(keys.contiguous(), None, None, vo, self.key_bits, self.sh)
         return vo.long()
 
     def bootstrap(self, points, weights):
