@@ -131,13 +131,16 @@ def device_workload(cfg, dev):
 
     c = CONFIGS[cfg]
     if cfg == "C5":
-        X = c5_device(n=c["n"], seed=0, device=dev)       # (2, n) SoA
-        pts_d = X.t()                                       # (n, 2) view, strides (1, n)
+        X = c5_device(n=c["n"], seed=0, device=dev)       # (2, n) as generated
+        # resident input in the reference's layout: a C-contiguous (n, 2) float64 array
+        # (the same layout the e2e call copies from the host)
+        pts_d = X.t().contiguous()
+        del X
+        torch.cuda.empty_cache()
 
         def host():
             h = torch.empty((c["n"], 2), dtype=torch.float64, pin_memory=True)
-            for j in range(2):
-                h[:, j].copy_(X[j])
+            h.copy_(pts_d)
             return h.numpy(), None
         return c, pts_d, None, host
     _, pts, w = workload(cfg)

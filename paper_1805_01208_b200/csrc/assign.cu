@@ -199,8 +199,8 @@ static AssignLayout assign_layout(int64_t m) {
   L.nregions = L.nchunks * (FCHUNK / WREG);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   size_t o = 0;
-  L.off_list = o; o = al(o + (size_t)L.nregions * WREG * 4);
-  L.off_olda = o; o = al(o + (size_t)L.nregions * WREG * 4);
+  L.off_list = o; o = al(o + (size_t)L.nregions * WREG * 8);   // int2 (position, old block)
+  L.off_olda = o;
   L.off_runs = o; o = al(o + (size_t)L.nregions * 4);
   L.off_sched = o; o = al(o + 8);
   L.total = o;
@@ -251,8 +251,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 template <int WM>
 __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshift, int64_t nchunks,
-                                                     int32_t* __restrict__ scan,
-                                                     int32_t* __restrict__ olda,
+                                                     int2* __restrict__ ent,
                                                      int32_t* __restrict__ runs,
                                                      unsigned long long* __restrict__ sched) {
   typedef typename std::conditional<WM == GP_W_UNIT, int, long long>::type RunW;
@@ -417,8 +416,7 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
       }
       // compaction of the points to scan into the region's own slots, in entry order
       // (entry 64h + 2l + b: ranks from two ballots per h)
-      int32_t* dst = scan + (int64_t)reg * WREG;
-      int32_t* dsa = olda + (int64_t)reg * WREG;
+      int2* dst = ent + (int64_t)reg * WREG;   // (position, old block): one 8-byte slot
       const unsigned lt = (1u << lane) - 1;
       int cnt = 0;
 #pragma unroll
@@ -427,14 +425,10 @@ __global__ void __launch_bounds__(FTH) filter_kernel(gp_assign_args p, int wshif
         const unsigned b0 = __ballot_sync(FULL, n0), b1 = __ballot_sync(FULL, n1);
         int off = cnt + __popc(b0 & lt) + __popc(b1 & lt);
         if (n0) {
-          dst[off] = q[2 * h];
-          dsa[off] = a[2 * h];  // the scan writes a only when the block changes
+          dst[off] = make_int2(q[2 * h], a[2 * h]);  // the scan writes a only on a change
           ++off;
         }
-        if (n1) {
-          dst[off] = q[2 * h + 1];
-          dsa[off] = a[2 * h + 1];
-        }
+        if (n1) dst[off] = make_int2(q[2 * h + 1], a[2 * h + 1]);
         cnt += __popc(b0) + __popc(b1);
       }
       if (lane == 0) runs[reg] = cnt;
@@ -666,8 +660,7 @@ constexpr int WKT = 256;
 
 template <int D, int WM>
 __global__ void __launch_bounds__(WKT) walk_kernel(gp_assign_args p, int wshift, int64_t nregions,
-                                                   const int32_t* __restrict__ scan,
-                                                   const int32_t* __restrict__ olda,
+                                                   const int2* __restrict__ ent,
                                                    const int32_t* __restrict__ runs) {
   typedef typename std::conditional<WM == GP_W_UNIT, int, long long>::type RunW;
   __shared__ WarpTab s_tab[WKT / 32];
@@ -683,7 +676,8 @@ __global__ void __launch_bounds__(WKT) walk_kernel(gp_assign_args p, int wshift,
     const int v = (int)(item - r * WREG);
     if (v >= runs[r]) continue;
     const int64_t slot = r * WREG + v;
-    const int q = scan[slot];
+    const int2 e = ent[slot];
+    const int q = e.x;
     double x[D];
     load_point<D>(p.X, p.ldx, q, x);
     int cc[3] = {0, 0, 0};
@@ -784,7 +778,7 @@ __global__ void __launch_bounds__(WKT) walk_kernel(gp_assign_args p, int wshift,
     }
     RunW wv = 0;
     if (lane == 0) {
-      if (olda[slot] != bi) p.a[q] = bi;
+      if (e.y != bi) p.a[q] = bi;
       store_bounds(p, lb_params(p, r * WREG), q, bi, bestf, secondf);
       wv = (RunW)weight_units<WM>(p.w, q, wshift);
     }
@@ -836,8 +830,7 @@ __device__ __forceinline__ void exact_argmin(const gp_assign_args& p, WarpCand<D
 
 template <int D, int WM>
 __global__ void __launch_bounds__(STH, GP_SCAN_OCC) scan_kernel(gp_assign_args p, int wshift, int64_t nregions,
-                                                   int sreg, const int32_t* __restrict__ scan,
-                                                   const int32_t* __restrict__ olda,
+                                                   int sreg, const int2* __restrict__ ent,
                                                    const int32_t* __restrict__ runs,
                                                    unsigned long long* __restrict__ sched,
                                                    int uch, int pshift) {
@@ -907,11 +900,12 @@ __global__ void __launch_bounds__(STH, GP_SCAN_OCC) scan_kernel(gp_assign_args p
       }
       return (unit * sreg + lo) * WREG + (v - rbeg[lo]);
     };
-    auto pos_of = [&](int v) { return scan[slot_of(v)]; };
+    auto pos_of = [&](int v) { return ent[slot_of(v)]; };   // (position, old block)
     // software pipeline of the passes: positions two passes ahead, coordinates one
     // pass ahead; the first pass's loads overlap the candidate selection below
-    int qA = p0 + lane < total_pts ? pos_of(p0 + lane) : 0;
-    int qB = p0 + pstride + lane < total_pts ? pos_of(p0 + pstride + lane) : 0;
+    const int2 zero2 = make_int2(0, -1);
+    int2 qA = p0 + lane < total_pts ? pos_of(p0 + lane) : zero2;
+    int2 qB = p0 + pstride + lane < total_pts ? pos_of(p0 + pstride + lane) : zero2;
     // candidate source: the group's hierarchical list, or all k centers
     if (p.group_list) {
       const int64_t g = (unit * sreg * WREG) >> p.group_shift;
@@ -940,7 +934,7 @@ __global__ void __launch_bounds__(STH, GP_SCAN_OCC) scan_kernel(gp_assign_args p
         hi[j] = -INFINITY;
       }
       for (int v = lane; v < total_pts; v += 32) {
-        const int q = pos_of(v);
+        const int q = pos_of(v).x;
         double xq[D];
         load_point<D>(p.X, p.ldx, q, xq);
 #pragma unroll
@@ -990,7 +984,7 @@ __global__ void __launch_bounds__(STH, GP_SCAN_OCC) scan_kernel(gp_assign_args p
     const bool overflow = ncand > CAPW;  // then stream the whole source in chunks
     const int total = overflow ? nsrc : ncand;
     double xA[D];
-    load_point<D>(p.X, p.ldx, qA, xA);  // first pass's coordinates (q = 0 when unused)
+    load_point<D>(p.X, p.ldx, qA.x, xA);  // first pass's coordinates (q = 0 when unused)
     if ((p.flags & 1) && lane == 0) {
       atomicAdd(&g_scan_stats[0], 1ull);
       atomicAdd(&g_scan_stats[1], (unsigned long long)total_pts);
@@ -1022,15 +1016,18 @@ __global__ void __launch_bounds__(STH, GP_SCAN_OCC) scan_kernel(gp_assign_args p
         const int v = vb + lane;
         const bool valid = v < total_pts;
         int bi = -1, q = 0;
+        int old = -1;
         if (valid) {
-          q = pos_of(v);
+          const int2 e = pos_of(v);
+          q = e.x;
+          old = e.y;
           double x[D];
           load_point<D>(p.X, p.ldx, q, x);
           float bestf, secondf;
           unsigned long long nn = 0;
           grid_point<D>(p, x, bi, bestf, secondf, nn);
           nq += nn;
-          if (olda[slot_of(v)] != bi) p.a[q] = bi;
+          if (old != bi) p.a[q] = bi;
           store_bounds(p, Lr, q, bi, bestf, secondf);
         }
         tab_add(tab, p.block_w, lane, valid, bi,
@@ -1042,15 +1039,15 @@ __global__ void __launch_bounds__(STH, GP_SCAN_OCC) scan_kernel(gp_assign_args p
     for (int pb = p0; pb < total_pts; pb += pstride) {
       const int v = pb + lane;
       const bool valid = v < total_pts;
-      const int q = valid ? qA : 0;
-      const int oa = valid ? olda[slot_of(v)] : -1;
+      const int q = valid ? qA.x : 0;
+      const int oa = valid ? qA.y : -1;
       double x[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) x[j] = xA[j];
       if (pb + pstride < total_pts) {
         qA = qB;
-        load_point<D>(p.X, p.ldx, qA, xA);
-        qB = pb + 2 * pstride + lane < total_pts ? pos_of(pb + 2 * pstride + lane) : 0;
+        load_point<D>(p.X, p.ldx, qA.x, xA);
+        qB = pb + 2 * pstride + lane < total_pts ? pos_of(pb + 2 * pstride + lane) : zero2;
       }
       // single pass: the two smallest q = d^2/infl^2 with their slots, and the third value
       double q1 = INFINITY, q2 = INFINITY, q3 = INFINITY;
@@ -1566,7 +1563,7 @@ static int g_sreg = 0;  // 0: automatic (GP_SCAN_REGIONS overrides)
 
 template <int WM>
 static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout& L,
-                         int32_t* scan, int32_t* olda, int32_t* runs,
+                         int2* ent, int32_t* runs,
                          unsigned long long* sched, cudaStream_t s) {
   static bool attr_set[3] = {false, false, false};
   const size_t fsm = (size_t)(FTH / 32) * FSTAGES * FREG_BYTES;
@@ -1575,7 +1572,7 @@ static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout
     attr_set[WM] = true;
   }
   unsigned gf = persistent_grid((const void*)filter_kernel<WM>, FTH, L.nchunks, fsm);
-  filter_kernel<WM><<<gf, FTH, fsm, s>>>(*a, wshift, L.nchunks, scan, olda, runs, sched);
+  filter_kernel<WM><<<gf, FTH, fsm, s>>>(*a, wshift, L.nchunks, ent, runs, sched);
   if (a->split_event) cudaEventRecord((cudaEvent_t)a->split_event, s);
   if (g_sreg == 0) {
     const char* e = getenv("GP_SCAN_REGIONS");
@@ -1612,20 +1609,20 @@ static void launch_round(const gp_assign_args* a, int wshift, const AssignLayout
     const unsigned gw = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((items + (WKT / 32) * 4 - 1) / ((WKT / 32) * 4), (int64_t)sms * 8));
     if (a->d == 2)
-      walk_kernel<2, WM><<<gw, WKT, 0, s>>>(*a, wshift, L.nregions, scan, olda, runs);
+      walk_kernel<2, WM><<<gw, WKT, 0, s>>>(*a, wshift, L.nregions, ent, runs);
     else
-      walk_kernel<3, WM><<<gw, WKT, 0, s>>>(*a, wshift, L.nregions, scan, olda, runs);
+      walk_kernel<3, WM><<<gw, WKT, 0, s>>>(*a, wshift, L.nregions, ent, runs);
     return;
   }
   unsigned gs;
   int uch, pshift;
   if (a->d == 2) {
     plan((const void*)scan_kernel<2, WM>, gs, uch, pshift);
-    scan_kernel<2, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs, sched,
+    scan_kernel<2, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, ent, runs, sched,
                                           uch, pshift);
   } else {
     plan((const void*)scan_kernel<3, WM>, gs, uch, pshift);
-    scan_kernel<3, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, scan, olda, runs, sched,
+    scan_kernel<3, WM><<<gs, STH, 0, s>>>(*a, wshift, L.nregions, sreg, ent, runs, sched,
                                           uch, pshift);
   }
 }
@@ -1661,14 +1658,13 @@ int gp_assign_round(const gp_assign_args* args, void* stream) {
   GP_REQUIRE(ldexp(1.0, wshift) == args->wscale, "gp_assign_round: wscale must be a power of 2");
   cudaStream_t s = (cudaStream_t)stream;
   char* ws = (char*)args->workspace;
-  int32_t* scan = (int32_t*)(ws + L.off_list);
-  int32_t* olda = (int32_t*)(ws + L.off_olda);
+  int2* ent = (int2*)(ws + L.off_list);
   int32_t* runs = (int32_t*)(ws + L.off_runs);
   unsigned long long* sched = (unsigned long long*)(ws + L.off_sched);
-  if (args->wmode == GP_W_UNIT) launch_round<GP_W_UNIT>(args, wshift, L, scan, olda, runs, sched, s);
+  if (args->wmode == GP_W_UNIT) launch_round<GP_W_UNIT>(args, wshift, L, ent, runs, sched, s);
   else if (args->wmode == GP_W_F32)
-    launch_round<GP_W_F32>(args, wshift, L, scan, olda, runs, sched, s);
-  else launch_round<GP_W_F64>(args, wshift, L, scan, olda, runs, sched, s);
+    launch_round<GP_W_F32>(args, wshift, L, ent, runs, sched, s);
+  else launch_round<GP_W_F64>(args, wshift, L, ent, runs, sched, s);
   return check_launch("assign_round");
 }
 

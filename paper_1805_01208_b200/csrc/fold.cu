@@ -143,22 +143,42 @@ __global__ void __launch_bounds__(RT) run_mark(gp_fold_args f, int64_t cnt, int6
     const int64_t wnext =
         wseg + 1 < GP_SEGMENTS ? ((int64_t)(wseg + 1) * f.n_global >> 8) - f.pos0 : INT64_MAX;
     const bool uni = p1 < wnext;
-    // carry: key of the entry before the current word (lane 0's predecessor)
+    // carry: key of the entry before the current word (lane 0's predecessor); inside
+    // the warp's segment it is hi | a (no segment search)
     int32_t carry = -2;
-    if (lane == 0 && wbase > 0) carry = entry_key(f, wbase - 1, f.a[wbase - 1], s0, bb);
     const int32_t hi = (int32_t)((wseg - s0) << bb);
-    if (uni) {
-      // keys = hi | a for a >= 0, -1 for a < 0: compare blocks, first word against carry
+    if (lane == 0 && wbase > 0) {
+      const int ap = f.a[wbase - 1];
+      const int64_t pp = f.list ? f.list[wbase - 1] : wbase - 1;
+      const int64_t sstart = ((int64_t)wseg * f.n_global >> 8) - f.pos0;
+      carry = pp >= sstart ? (ap < 0 ? -1 : (hi | ap)) : entry_key(f, wbase - 1, ap, s0, bb);
+    }
+    if (uni && whole) {
+      // keys = hi | a for a >= 0, -1 for a < 0: compare blocks, first word against carry;
+      // lane t keeps word t, and the warp stores its 16 words at once
+      unsigned mine = 0;
 #pragma unroll
       for (int t = 0; t < NW; ++t) {
         const int32_t key = av[t] < 0 ? -1 : (hi | av[t]);
         int32_t prev = __shfl_up_sync(FULL, key, 1);
         if (lane == 0) prev = carry;
         carry = __shfl_sync(FULL, key, 31);
-        const bool in = whole || wbase + 32 * t + lane < cnt;
+        const unsigned word = __ballot_sync(FULL, key != prev);
+        if (lane == t) mine = word;
+      }
+      if (lane < NW) mask[(wbase >> 5) + lane] = mine;
+      total = __reduce_add_sync(FULL, lane < NW ? __popc(mine) : 0u);
+    } else if (uni) {
+#pragma unroll
+      for (int t = 0; t < NW; ++t) {
+        const int32_t key = av[t] < 0 ? -1 : (hi | av[t]);
+        int32_t prev = __shfl_up_sync(FULL, key, 1);
+        if (lane == 0) prev = carry;
+        carry = __shfl_sync(FULL, key, 31);
+        const bool in = wbase + 32 * t + lane < cnt;
         const unsigned word = __ballot_sync(FULL, in && key != prev);
         total += __popc(word);
-        if (lane == 0 && (whole || wbase + 32 * t < cnt)) mask[(wbase >> 5) + t] = word;
+        if (lane == 0 && wbase + 32 * t < cnt) mask[(wbase >> 5) + t] = word;
       }
     } else {
       for (int t = 0; t < NW; ++t) {
