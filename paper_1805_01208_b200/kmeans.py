@@ -1326,6 +1326,24 @@ def balanced_kmeans(graph, settings: KMeansSettings, world: RankWorld | None = N
         raise ValueError("world does not match the graph")
     # the reference runs the pipeline on the world's own shards (kmeans.py:531-534), so a
     # world built from other coordinates or weights (same n) partitions those
-    coords = world.coords if world.coords is not None else graph.coords
-    return balanced_kmeans_points(coords, world.weights, settings, p=world.p,
+    coords, weights = _world_arrays(world, graph)
+    return balanced_kmeans_points(coords, weights, settings, p=world.p,
                                   return_stats=return_stats)
+
+
+def _world_arrays(world, graph):
+    """(coords, weights) a world partitions: this module's RankWorld carries them; a
+    reference ``ranksim.RankWorld`` (reached through the INTEGRATION.md shim, e.g. from
+    ``cli.py:110-111``) holds them as shards whose gids index the original rows
+    (``ranksim.py:53-108``)."""
+    shards = getattr(world, "shards", None)
+    if shards is None:
+        return (world.coords if world.coords is not None else graph.coords), world.weights
+    n, d = int(world.n), int(world.dim)
+    coords = np.empty((n, d), dtype=np.float64)
+    weights = np.empty(n, dtype=np.float64)
+    for sh in shards:
+        g = np.asarray(sh.gids, dtype=np.int64)
+        coords[g] = np.asarray(sh.points, dtype=np.float64)
+        weights[g] = np.asarray(sh.weights, dtype=np.float64)
+    return coords, weights
