@@ -44,35 +44,20 @@ def tests_dir(arg: str | None) -> str | None:
 
 
 class Shim:
-    """Route the reference's entry points to the B200 ones and count the calls."""
-
-    NAMES = ("balanced_kmeans_points", "balanced_kmeans")
+    """Route the reference's entry points to the B200 ones (the package's own
+    `integration.install`, i.e. the INTEGRATION.md shim) and count the calls."""
 
     def __init__(self):
-        self.calls = {n: 0 for n in self.NAMES}
-        self.ref = {}
+        self.calls = {"balanced_kmeans_points": 0, "balanced_kmeans": 0}
 
     def install(self):
         import geopart  # noqa: F401  (the reference, from baseline/_ref)
         import geopart.cli  # noqa: F401
         import geopart.estimators  # noqa: F401
-        import geopart.kmeans as rk
 
-        from paper_1805_01208_b200 import kmeans as bk
+        from paper_1805_01208_b200 import integration
 
-        for name in self.NAMES:
-            ref_fn, b200_fn = getattr(rk, name), getattr(bk, name)
-            self.ref[name] = ref_fn
-
-            def wrapped(*a, _f=b200_fn, _n=name, **kw):
-                self.calls[_n] += 1
-                return _f(*a, **kw)
-
-            wrapped.__doc__ = b200_fn.__doc__
-            for mod in list(sys.modules.values()):
-                if getattr(mod, "__name__", "").split(".")[0] == "geopart" and \
-                        getattr(mod, name, None) is ref_fn:
-                    setattr(mod, name, wrapped)
+        integration.install(counter=self.calls)
 
 
 def main(argv=None) -> int:
