@@ -77,9 +77,12 @@ int gp_hilbert_keys(const double* pts, int64_t n, int d, int64_t stride_pt, int6
  * algorithm as the kernel; used by the host-logic tests. */
 uint64_t gp_hilbert_cell_key_host(const uint32_t* cells, int d, int depth);
 
-/* K3  stable LSD radix sort of (key, gid) pairs on the low key_bits bits:
+/* K3  stable radix sort of (key, gid) pairs on the low key_bits bits:
  * replaces np.lexsort((gids, keys)) in ranksim.py:158 (gids arrive in
- * increasing order, so a stable key sort is the same total order). */
+ * increasing order, so a stable key sort is the same total order).  Hand-written
+ * (csrc/radix.cu): onesweep LSD passes over the top key bits, then one pass that
+ * orders each top-bits bucket by the full key.  vals_in NULL: val = input position.
+ * keys_out must not alias keys_in; the inputs are left intact. */
 int gp_sort_workspace_bytes(int64_t n, size_t* bytes);
 int gp_sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
                   uint32_t* vals_out, int64_t n, int key_bits, void* workspace,

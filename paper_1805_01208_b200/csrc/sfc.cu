@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "radix.cuh"
 
 namespace gp {
 
@@ -592,15 +593,7 @@ uint64_t gp_hilbert_cell_key_host(const uint32_t* cells, int d, int depth) {
 
 int gp_sort_workspace_bytes(int64_t n, size_t* bytes) {
   GP_REQUIRE(n >= 0 && n < (1ll << 31), "gp_sort: n out of range");
-  size_t b = 0;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint64_t*)nullptr,
-                                                  (uint64_t*)nullptr, (const uint32_t*)nullptr,
-                                                  (uint32_t*)nullptr, (int)n, 0, 64);
-  if (e != cudaSuccess) {
-    set_error("sort workspace query failed: %s", cudaGetErrorString(e));
-    return GP_ERR_CUDA;
-  }
-  *bytes = b;
+  *bytes = radix::workspace_bytes(n, 8, 4);
   return GP_OK;
 }
 
@@ -608,12 +601,9 @@ int gp_sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* ke
                   uint32_t* vals_out, int64_t n, int key_bits, void* workspace,
                   size_t workspace_bytes, void* stream) {
   GP_REQUIRE(key_bits >= 1 && key_bits <= 64, "gp_sort: key_bits out of range");
-  GP_REQUIRE(n >= 0 && n < (1ll << 31), "gp_sort: n out of range");
-  if (n == 0) return GP_OK;
-  size_t b = workspace_bytes;
-  GP_CUDA(cub::DeviceRadixSort::SortPairs(workspace, b, keys_in, keys_out, vals_in, vals_out,
-                                          (int)n, 0, key_bits, (cudaStream_t)stream));
-  return check_launch("sort_pairs");
+  return radix::sort_pairs<uint64_t, uint32_t>(keys_in, vals_in, keys_out, vals_out, n, 0,
+                                               key_bits, workspace, workspace_bytes,
+                                               (cudaStream_t)stream, true);
 }
 
 int gp_gather_points(const double* pts, int64_t stride_pt, int64_t stride_dim, int d,
