@@ -400,6 +400,121 @@ int gp_sfc_cut(const uint32_t* gids, const double* w, int64_t n, int k, double s
 int gp_predict(const double* X, int64_t n, int d, const double* centers, const double* influence,
                int k, int safe_influence, int64_t* labels, void* stream);
 
+/* ---- formats and evaluation either side of the path -------- */
+
+/* token kinds written by gp_text_tokens */
+#define GP_TOK_INT 0     /* [+-]?digits, at most 18 significant: value = the int64 */
+#define GP_TOK_REAL 1    /* plain decimal real: value = bits of the correctly rounded double */
+#define GP_TOK_PERCENT 2 /* starts with '%' (a METIS comment line when first on its line) */
+#define GP_TOK_SUSPECT 3 /* anything else (nan, 1_000, > 19 digits, ...): the host decides */
+
+/* Host helper (host pointers): the tokenizer's number conversion for one token; returns
+ * the kind.  Used by the CPU tests to pin the decimal -> binary64 conversion to Python's
+ * float() without a GPU. */
+int gp_parse_number_host(const char* text, int len, int64_t* value);
+
+/* Line and token index of a text file held in device memory (fileio.py:83 `f.read()
+ * .splitlines()` + `line.split()`, and np.loadtxt's rows in fileio.py:222, :250).
+ * Lines end at '\n', '\r\n' or a lone '\r'; tokens are separated by blanks and tabs.
+ * comment_char != 0 ('#' for the np.loadtxt formats): the rest of a line from that
+ * character is ignored.  gp_text_index writes counts[0..3) = {lines, tokens, bytes that
+ * are not printable ASCII, tab or a line end} (device); after reading them the caller sizes the outputs of gp_text_tokens:
+ *   line_off[l]  (lines + 1)  byte offset of line l (sentinel: len)
+ *   line_tok0[l] (lines + 1)  index of the first token at or after line l (sentinel: tokens)
+ *   tok_val / tok_kind (tokens)  value and GP_TOK_* kind of every token
+ * The same workspace (gp_text_index_workspace_bytes) must be passed to both calls. */
+int gp_text_index_workspace_bytes(int64_t len, size_t* bytes);
+int gp_text_index(const uint8_t* text, int64_t len, int comment_char, int64_t* counts,
+                  void* workspace, size_t workspace_bytes, void* stream);
+int gp_text_tokens(const uint8_t* text, int64_t len, int comment_char, const void* workspace,
+                   int64_t n_lines, int64_t n_tokens, int64_t* line_off, int64_t* line_tok0,
+                   int64_t* tok_val, uint8_t* tok_kind, void* stream);
+
+/* METIS adjacency file -> CSR (fileio.py:70-170).
+ * gp_metis_lines: drops '%' comment lines (fileio.py:85-93); info (device) = {non-comment
+ *   lines, line of the header, 1 + index of the last vertex line holding a token};
+ *   body_line[v] = line of vertex v (the v+1-th non-comment line after the header).
+ * gp_metis_offsets: offsets[0..n] from the token counts (fileio.py:131-149, :163-164);
+ *   flags[v] = 1 where the line lacks its vertex weight or ends in a dangling neighbor.
+ * gp_metis_fill: neighbors (0-based), edge and vertex weights; flags[v] |= 1 for every
+ *   line the reference rejects for a bad token, an id out of range, a self loop or a
+ *   non-positive weight.  Flagged lines are re-read by the host for the message (and for
+ *   tokens only Python's int()/float() accept).  Duplicates are left to gp_graph_check. */
+int gp_metis_workspace_bytes(int64_t n_lines, size_t* bytes);
+int gp_metis_lines(const int64_t* line_tok0, const uint8_t* tok_kind, int64_t n_lines,
+                   int64_t* body_line, int64_t body_cap, int64_t* info, void* workspace,
+                   size_t workspace_bytes, void* stream);
+int gp_metis_offsets(const int64_t* line_tok0, const int64_t* body_line, int64_t n, int has_vw,
+                     int has_ew, int64_t* offsets, uint8_t* flags, void* workspace,
+                     size_t workspace_bytes, void* stream);
+int gp_metis_fill(const int64_t* line_tok0, const int64_t* body_line, const int64_t* tok_val,
+                  const uint8_t* tok_kind, int64_t n, int has_vw, int has_ew,
+                  const int64_t* offsets, int64_t* neighbors, double* edge_weights,
+                  double* vertex_weights, uint8_t* flags, void* stream);
+
+/* Whitespace table (np.loadtxt in fileio.py:222 and :250): out[t] = value of token t as
+ * double (want_int 0) or int64 (want_int 1) -- the row-major table once every non-blank
+ * line has as many tokens as the first.  info (device) = {rows, first line with another
+ * token count or -1, first token that is not a plain number of the wanted type or -1,
+ * columns}. */
+int gp_table_values(const int64_t* line_tok0, int64_t n_lines, const int64_t* tok_val,
+                    const uint8_t* tok_kind, int64_t n_tokens, int want_int, void* out,
+                    int64_t* info, void* stream);
+
+/* Partition writer (fileio.py:271-278): one decimal per line.  _plan computes the byte
+ * position of every value and *out_len (device); _write fills out[0, out_len) using the
+ * same workspace. */
+int gp_format_ints_workspace_bytes(int64_t n, size_t* bytes);
+int gp_format_ints_plan(const int64_t* values, int64_t n, int64_t* out_len, void* workspace,
+                        size_t workspace_bytes, void* stream);
+int gp_format_ints_write(const int64_t* values, int64_t n, uint8_t* out, const void* workspace,
+                         void* stream);
+
+/* Structural check of a CSR graph (graph.py:85-128, fileio.py:173-187).  result (device):
+ * result[0] = bit flags {1 neighbor out of range, 2 self loop, 4 parallel edge,
+ * 8 asymmetric, 16 edge weight differs between directions, 32 non-positive edge weight,
+ * 64 offsets malformed}; result[1] = the smallest directed-edge key u*n+v whose reverse
+ * is missing (fileio.py:180-183), or -1.  vertex_flags (nullable, n bytes): set to 1 for
+ * every vertex listing a neighbor twice. */
+int gp_graph_check_workspace_bytes(int64_t nnz, size_t* bytes);
+int gp_graph_check(const int64_t* offsets, const int64_t* neighbors, const double* edge_weights,
+                   int64_t n, int64_t nnz, uint8_t* vertex_flags, int64_t* result,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* metrics.py:48-60.  edge_weights NULL: the number of cut edges.  scale > 0: every edge
+ * weight times scale is an exact integer (gp_weight_probe) and the cut is summed in
+ * int64; scale == 0: numpy's pairwise sum of the masked weights in CSR order (this
+ * variant synchronises the stream).  *out is a device double. */
+int gp_edge_cut_workspace_bytes(int64_t n, int64_t nnz, size_t* bytes);
+int gp_edge_cut(const int64_t* offsets, const int64_t* neighbors, const double* edge_weights,
+                double scale, const int32_t* assignment, int64_t n, int64_t nnz, double* out,
+                void* workspace, size_t workspace_bytes, void* stream);
+
+/* metrics.py:63-77: per_block[b] = sum over the vertices of block b of the number of other
+ * blocks among their neighbors.  heavy_scratch: n + 1 int64. */
+int gp_comm_volumes(const int64_t* offsets, const int64_t* neighbors, const int32_t* assignment,
+                    int64_t n, int k, int64_t* per_block, int64_t* heavy_scratch, void* stream);
+
+/* graph.py:165-166: np.bincount(assignment, weights, minlength=k).  weights NULL = ones.
+ * scale > 0: exact integer units; scale == 0: the sequential fold in vertex order. */
+int gp_block_weights_workspace_bytes(int64_t n, int k, size_t* bytes);
+int gp_block_weights(const double* weights, const int32_t* assignment, int64_t n, int k,
+                     double scale, double* out, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+/* metrics.py:80-168: BFS inside every block at once from roots[b] (-1 = none), hop levels
+ * into level (int32, -1 = unreached).  changed: 8 device int32 of scratch.  Synchronises the
+ * stream (reads the progress flag every 8 levels).
+ * gp_block_level_top: out[b] = max over the block's vertices v != exclude[b] with key <
+ * below[b] of key = (level + 1) << 32 | (2^32 - 1 - v), i.e. the deepest vertex, lowest id
+ * first (metrics.py:115-118, :152); unreached[b] (nullable) = vertices of b with level -1. */
+int gp_block_bfs(const int64_t* offsets, const int64_t* neighbors, const int32_t* assignment,
+                 int64_t n, int k, const int64_t* roots, int32_t* level, int32_t* changed,
+                 int32_t* depth, void* stream);
+int gp_block_level_top(const int32_t* level, const int32_t* assignment, int64_t n, int k,
+                       const int64_t* exclude, const uint64_t* below, uint64_t* out,
+                       uint64_t* unreached, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

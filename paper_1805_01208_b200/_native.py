@@ -101,6 +101,28 @@ _SIGS = {
     "gp_sfc_cut_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_sfc_cut": (C.c_int, [vp, vp, i64, C.c_int, f64, vp, vp, sz, vp]),
     "gp_predict": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]),
+    # formats and evaluation either side of the path (csrc/textio.cu, csrc/graphs.cu)
+    "gp_parse_number_host": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(i64)]),
+    "gp_text_index_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_text_index": (C.c_int, [vp, i64, C.c_int, vp, vp, sz, vp]),
+    "gp_text_tokens": (C.c_int, [vp, i64, C.c_int, vp, i64, i64, vp, vp, vp, vp, vp]),
+    "gp_metis_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_metis_lines": (C.c_int, [vp, vp, i64, vp, i64, vp, vp, sz, vp]),
+    "gp_metis_offsets": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, vp, vp, vp, sz, vp]),
+    "gp_metis_fill": (C.c_int, [vp, vp, vp, vp, i64, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]),
+    "gp_table_values": (C.c_int, [vp, i64, vp, vp, i64, C.c_int, vp, vp, vp]),
+    "gp_format_ints_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_format_ints_plan": (C.c_int, [vp, i64, vp, vp, sz, vp]),
+    "gp_format_ints_write": (C.c_int, [vp, i64, vp, vp, vp]),
+    "gp_graph_check_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_graph_check": (C.c_int, [vp, vp, vp, i64, i64, vp, vp, vp, sz, vp]),
+    "gp_edge_cut_workspace_bytes": (C.c_int, [i64, i64, C.POINTER(sz)]),
+    "gp_edge_cut": (C.c_int, [vp, vp, vp, f64, vp, i64, i64, vp, vp, sz, vp]),
+    "gp_comm_volumes": (C.c_int, [vp, vp, vp, i64, C.c_int, vp, vp, vp]),
+    "gp_block_weights_workspace_bytes": (C.c_int, [i64, C.c_int, C.POINTER(sz)]),
+    "gp_block_weights": (C.c_int, [vp, vp, i64, C.c_int, f64, vp, vp, sz, vp]),
+    "gp_block_bfs": (C.c_int, [vp, vp, vp, i64, C.c_int, vp, vp, vp, vp, vp]),
+    "gp_block_level_top": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -142,6 +164,10 @@ KERNELS_PER_CALL = {
     "gp_group_boxes": 1,
     "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 3, "gp_region_maps": 1, "gp_lb_remap": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
     "gp_sfc_cut": 3, "gp_predict": 1, "gp_balance_decide": 1, "gp_center_grid": 3,
+    "gp_text_index": 2, "gp_text_tokens": 1, "gp_metis_lines": 3, "gp_metis_offsets": 2,
+    "gp_metis_fill": 1, "gp_table_values": 3, "gp_format_ints_plan": 2,
+    "gp_format_ints_write": 1, "gp_graph_check": 22, "gp_edge_cut": 2, "gp_comm_volumes": 2,
+    "gp_block_weights": 2, "gp_block_bfs": 9, "gp_block_level_top": 1,
 }
 _launches = [0]
 calls: dict[str, int] = {}   # API calls by name (tools/kprof.py)

@@ -184,6 +184,16 @@ static int pairwise_depth(int64_t n) {
   return L;
 }
 
+// numpy's pairwise sum of a[0, n) into *total (part: 4096 doubles of scratch); shared with
+// graphs.cu (the weighted edge cut)
+int pairwise_sum_async(const double* a, int64_t n, double* part, double* total, cudaStream_t s) {
+  const int L = pairwise_depth(n);
+  const int m = 1 << L;
+  pairwise_subtrees_kernel<<<(m + 127) / 128, 128, 0, s>>>(a, n, L, part);
+  pairwise_top_kernel<<<1, 256, m * sizeof(double), s>>>(part, L, total);
+  return check_launch("pairwise_sum");
+}
+
 static unsigned sm_grid(int64_t n, int per) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
