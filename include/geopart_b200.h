@@ -503,14 +503,17 @@ int gp_block_weights(const double* weights, const int32_t* assignment, int64_t n
                      void* stream);
 
 /* metrics.py:80-168: BFS inside every block at once from roots[b] (-1 = none), hop levels
- * into level (int32, -1 = unreached).  changed: 8 device int32 of scratch.  Synchronises the
- * stream (reads the progress flag every 8 levels).
+ * into level (int32, -1 = unreached); one CTA per block, one launch per sweep.  qbase
+ * (k + 1) = exclusive prefix sums of the block sizes; queue = n int64 of scratch.  Per
+ * block: depth[b] = the largest level, far[b] = the lowest vertex id on it
+ * (metrics.py:115-118), reached[b] = vertices reached (a block is connected iff it equals
+ * the block size).
  * gp_block_level_top: out[b] = max over the block's vertices v != exclude[b] with key <
  * below[b] of key = (level + 1) << 32 | (2^32 - 1 - v), i.e. the deepest vertex, lowest id
- * first (metrics.py:115-118, :152); unreached[b] (nullable) = vertices of b with level -1. */
+ * first (metrics.py:152); unreached[b] (nullable) = vertices of b with level -1. */
 int gp_block_bfs(const int64_t* offsets, const int64_t* neighbors, const int32_t* assignment,
-                 int64_t n, int k, const int64_t* roots, int32_t* level, int32_t* changed,
-                 int32_t* depth, void* stream);
+                 int64_t n, int k, const int64_t* roots, const int64_t* qbase, int64_t* queue,
+                 int32_t* level, int32_t* depth, int64_t* far, int64_t* reached, void* stream);
 int gp_block_level_top(const int32_t* level, const int32_t* assignment, int64_t n, int k,
                        const int64_t* exclude, const uint64_t* below, uint64_t* out,
                        uint64_t* unreached, void* stream);

@@ -121,7 +121,7 @@ _SIGS = {
     "gp_comm_volumes": (C.c_int, [vp, vp, vp, i64, C.c_int, vp, vp, vp]),
     "gp_block_weights_workspace_bytes": (C.c_int, [i64, C.c_int, C.POINTER(sz)]),
     "gp_block_weights": (C.c_int, [vp, vp, i64, C.c_int, f64, vp, vp, sz, vp]),
-    "gp_block_bfs": (C.c_int, [vp, vp, vp, i64, C.c_int, vp, vp, vp, vp, vp]),
+    "gp_block_bfs": (C.c_int, [vp, vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp]),
     "gp_block_level_top": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp]),
 }
 
@@ -167,7 +167,7 @@ KERNELS_PER_CALL = {
     "gp_text_index": 2, "gp_text_tokens": 1, "gp_metis_lines": 3, "gp_metis_offsets": 2,
     "gp_metis_fill": 1, "gp_table_values": 3, "gp_format_ints_plan": 2,
     "gp_format_ints_write": 1, "gp_graph_check": 22, "gp_edge_cut": 2, "gp_comm_volumes": 2,
-    "gp_block_weights": 2, "gp_block_bfs": 9, "gp_block_level_top": 1,
+    "gp_block_weights": 2, "gp_block_bfs": 1, "gp_block_level_top": 1,
 }
 _launches = [0]
 calls: dict[str, int] = {}   # API calls by name (tools/kprof.py)

@@ -10,7 +10,7 @@
 //   gp_block_weights   graph.py:165-166 (np.bincount with weights): exact int64 units,
 //                      or the sequential per-block fold in vertex order
 //   gp_block_bfs,      metrics.py:121-168: the per-block BFS sweeps run for ALL blocks at
-//   gp_block_level_top once (edges leaving a block are ignored), level-synchronous
+//   gp_block_level_top once (edges leaving a block are ignored), one CTA per block
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
@@ -294,23 +294,68 @@ __global__ void block_fold(const unsigned* __restrict__ order, const long long* 
 }
 
 // ---------------------------------------------------------------- per-block BFS
-__global__ void bfs_init(const long long* __restrict__ roots, int k, int* __restrict__ level) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k; b += gridDim.x * blockDim.x)
-    if (roots[b] >= 0) level[roots[b]] = 0;
-}
-__global__ void bfs_step(const long long* __restrict__ off, const long long* __restrict__ nbr,
-                         const int* __restrict__ a, long long n, int d, int* __restrict__ level,
-                         int* __restrict__ changed) {
-  bool any = false;
-  VERTEX_LOOP(u, n) {
-    if (level[u] != d) continue;
-    const int au = a[u];
-    for (long long j = off[u]; j < off[u + 1]; ++j) {
-      const long long v = nbr[j];
-      if (a[v] == au && level[v] < 0) { level[v] = d + 1; any = true; }
+// One CTA per block (blocks are independent: edges leaving a block are ignored), so a
+// sweep of ALL blocks is one launch with no grid-wide step per level.  The CTA keeps the
+// block's frontier queue in global memory (a block's vertices enter it exactly once, so
+// block b owns queue[qbase[b], qbase[b + 1])), claims unvisited neighbors with an
+// atomicCAS on their level and synchronises its own levels with __syncthreads.
+constexpr int BFS_THREADS = 512;
+
+__global__ void __launch_bounds__(BFS_THREADS) bfs_blocks(
+    const long long* __restrict__ off, const long long* __restrict__ nbr,
+    const int* __restrict__ a, int k, const long long* __restrict__ roots,
+    const long long* __restrict__ qbase, long long* __restrict__ queue, int* __restrict__ level,
+    int* __restrict__ depth, long long* __restrict__ far, long long* __restrict__ reached) {
+  __shared__ long long s_head, s_tail, s_next;
+  __shared__ unsigned long long s_far;
+  for (int b = blockIdx.x; b < k; b += gridDim.x) {
+    const long long root = roots[b];
+    if (root < 0) {
+      if (threadIdx.x == 0) { depth[b] = -1; far[b] = -1; reached[b] = 0; }
+      continue;
     }
+    long long* q = queue + qbase[b];
+    __syncthreads();  // the previous block's reads of the shared cursors are done
+    if (threadIdx.x == 0) {
+      q[0] = root;
+      level[root] = 0;
+      s_head = 0; s_tail = 1; s_next = 1;
+    }
+    __syncthreads();
+    int d = 0;
+    long long head = 0, tail = 1;
+    for (;;) {
+      for (long long i = head + threadIdx.x; i < tail; i += BFS_THREADS) {
+        const long long u = q[i];
+        for (long long j = off[u]; j < off[u + 1]; ++j) {
+          const long long v = nbr[j];
+          if (a[v] != b || level[v] >= 0) continue;
+          if (atomicCAS(&level[v], -1, d + 1) == -1)
+            q[atomicAdd((unsigned long long*)&s_next, 1ull)] = v;
+        }
+      }
+      __syncthreads();
+      const long long next = s_next;
+      if (next == tail) break;  // no deeper level: [head, tail) is the deepest one
+      head = tail;
+      tail = next;
+      ++d;
+      __syncthreads();
+    }
+    // deepest level: its lowest vertex id (metrics.py:115-118)
+    if (threadIdx.x == 0) s_far = ~0ull;
+    __syncthreads();
+    unsigned long long mine = ~0ull;
+    for (long long i = head + threadIdx.x; i < tail; i += BFS_THREADS)
+      mine = (unsigned long long)q[i] < mine ? (unsigned long long)q[i] : mine;
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(FULL, mine, o);
+      mine = other < mine ? other : mine;
+    }
+    if ((threadIdx.x & 31) == 0 && mine != ~0ull) atomicMin(&s_far, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) { depth[b] = d; far[b] = (long long)s_far; reached[b] = tail; }
   }
-  if (any) *changed = 1;
 }
 
 // per block: the largest key (level + 1) << 32 | (2^32 - 1 - vertex) over its vertices
@@ -515,27 +560,19 @@ int gp_block_weights(const double* weights, const int32_t* assignment, int64_t n
 }
 
 int gp_block_bfs(const int64_t* offsets, const int64_t* neighbors, const int32_t* assignment,
-                 int64_t n, int k, const int64_t* roots, int32_t* level, int32_t* changed,
-                 int32_t* depth, void* stream) {
+                 int64_t n, int k, const int64_t* roots, const int64_t* qbase, int64_t* queue,
+                 int32_t* level, int32_t* depth, int64_t* far, int64_t* reached, void* stream) {
   GP_REQUIRE(n >= 1 && k >= 1, "gp_block_bfs: sizes out of range");
   cudaStream_t s = (cudaStream_t)stream;
   GP_CUDA(cudaMemsetAsync(level, 0xff, (size_t)n * 4, s));
-  bfs_init<<<grid_for(k, 256), 256, 0, s>>>((const long long*)roots, k, level);
-  const unsigned g = sm_grid(n, 128);
-  int d = 0;
-  // level-synchronous sweeps, 8 levels per read-back of the progress flag
-  for (;;) {
-    GP_CUDA(cudaMemsetAsync(changed, 0, 8 * sizeof(int), s));
-    for (int i = 0; i < 8; ++i, ++d)
-      bfs_step<<<g, 128, 0, s>>>((const long long*)offsets, (const long long*)neighbors,
-                                 assignment, n, d, level, changed + i);
-    int h[8];
-    GP_CUDA(cudaMemcpyAsync(h, changed, sizeof(h), cudaMemcpyDeviceToHost, s));
-    GP_CUDA(cudaStreamSynchronize(s));
-    if (!h[7]) break;
-    GP_REQUIRE(d < (1 << 30), "gp_block_bfs: runaway");
-  }
-  if (depth) *depth = d;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = k < sms * 4 ? k : sms * 4;
+  bfs_blocks<<<grid, BFS_THREADS, 0, s>>>((const long long*)offsets, (const long long*)neighbors,
+                                          assignment, k, (const long long*)roots,
+                                          (const long long*)qbase, (long long*)queue, level,
+                                          depth, (long long*)far, (long long*)reached);
   return check_launch("gp_block_bfs");
 }
 

@@ -482,15 +482,25 @@ __global__ void metis_body_lines(const long long* __restrict__ rank_excl,
                                  const long long* __restrict__ line_tok0, long long n_lines,
                                  long long* __restrict__ body_line, long long body_cap,
                                  long long* __restrict__ info) {
+  unsigned long long last = 0;  // 1 + largest vertex index whose line holds a token
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < n_lines;
        l += (long long)gridDim.x * blockDim.x) {
     if (!body_flag[l]) continue;
     const long long r = rank_excl[l];
     if (r == 0) { info[1] = l; continue; }
     if (r - 1 < body_cap) body_line[r - 1] = l;
-    if (line_tok0[l + 1] > line_tok0[l])
-      atomicMax((unsigned long long*)&info[2], (unsigned long long)(r - 1 + 1));
+    if (line_tok0[l + 1] > line_tok0[l] && (unsigned long long)r > last) last = r;
   }
+  __shared__ unsigned long long s_last;
+  if (threadIdx.x == 0) s_last = 0;
+  __syncthreads();
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(FULL, last, o);
+    last = other > last ? other : last;
+  }
+  if ((threadIdx.x & 31) == 0 && last) atomicMax(&s_last, last);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_last) atomicMax((unsigned long long*)&info[2], s_last);
 }
 
 // degrees (fileio.py:131-149): tokens minus the optional weight, halved with edge weights

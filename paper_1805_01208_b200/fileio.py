@@ -114,6 +114,17 @@ def _tokenize(buf: np.ndarray, comment_char: int) -> _Tokens:
     return _Tokens(buf, n_lines, n_tokens, line_off, line_tok0, tok_val, tok_kind)
 
 
+def _to_host(t) -> np.ndarray:
+    """A device tensor as a numpy array, through the pinned staging ring."""
+    from . import staging
+
+    out = np.empty(tuple(t.shape), dtype={"torch.int64": np.int64, "torch.float64": np.float64,
+                                          "torch.uint8": np.uint8}[str(t.dtype)])
+    if out.size:
+        staging.d2h_into(out, t.contiguous())
+    return out
+
+
 # ---------------------------------------------------------------- METIS graph
 def _fail(lineno, msg):
     raise MetisParseError(f"line {lineno}: {msg}")
@@ -285,9 +296,9 @@ def load_metis_graph(graph_source, coord_source=None) -> GeometricGraph:
         coords = np.zeros((n, 2), dtype=np.float64)
     else:
         coords = load_coords(coord_source, expect_n=n)
-    g = GeometricGraph(offsets.cpu().numpy(), neighbors.cpu().numpy(), coords,
-                       np.ones(n, dtype=np.float64) if vw is None else vw.cpu().numpy(),
-                       None if ew is None else ew.cpu().numpy())
+    g = GeometricGraph(_to_host(offsets), _to_host(neighbors), coords,
+                       np.ones(n, dtype=np.float64) if vw is None else _to_host(vw),
+                       None if ew is None else _to_host(ew))
     g.validate(_checked=chk)
     return g
 
@@ -378,7 +389,7 @@ def read_partition(source, expect_n: int | None = None, k: int | None = None) ->
     else:
         if rows > 1 and ncols > 1:
             raise MetisParseError("partition file must hold one block id per line")
-        a = vals.cpu().numpy()
+        a = _to_host(vals)
     if expect_n is not None and a.shape[0] != expect_n:
         raise MetisParseError(f"partition file has {a.shape[0]} lines, expected {expect_n}")
     if a.size and int(vals.min().item()) < 0:

@@ -169,44 +169,47 @@ def block_diameter_lower_bounds(graph, partition: Partition,
     g = _on_device(graph, partition)
     k, n, sh = g.k, g.n, _stream()
     level = torch.empty(n, dtype=torch.int32, device="cuda")
-    changed = torch.empty(8, dtype=torch.int32, device="cuda")
     key = torch.empty(k, dtype=torch.int64, device="cuda")      # uint64 bit patterns < 2^63
-    unreached = torch.empty(k, dtype=torch.int64, device="cuda")
     LOW = (1 << 32) - 1
+    sizes = torch.bincount(g.labels.to(torch.int64), minlength=k)
+    qbase = torch.zeros(k + 1, dtype=torch.int64, device="cuda")
+    qbase[1:] = torch.cumsum(sizes, 0)
+    queue = torch.empty(n, dtype=torch.int64, device="cuda")
 
-    def bfs(roots):
+    def bfs(roots, lev):
+        """one sweep of every block: (largest level, its lowest vertex, vertices reached)"""
+        depth = torch.empty(k, dtype=torch.int32, device="cuda")
+        far = torch.empty(k, dtype=torch.int64, device="cuda")
+        reached = torch.empty(k, dtype=torch.int64, device="cuda")
         N.call("gp_block_bfs", g.offsets.data_ptr(), g.neighbors.data_ptr(), g.labels.data_ptr(),
-               n, k, roots.data_ptr(), level.data_ptr(), changed.data_ptr(), None, sh)
+               n, k, roots.data_ptr(), qbase.data_ptr(), queue.data_ptr(), lev.data_ptr(),
+               depth.data_ptr(), far.data_ptr(), reached.data_ptr(), sh)
+        return depth.to(torch.int64), far, reached
 
-    def top(lev, exclude=None, below=None, count_unreached=False):
-        """per block: (key, level, vertex) of the deepest vertex, lowest id first"""
+    def top(lev, exclude=None, below=None):
+        """per block: (key, vertex) of the deepest vertex, lowest id first"""
         N.call("gp_block_level_top", lev.data_ptr(), g.labels.data_ptr(), n, k,
                None if exclude is None else exclude.data_ptr(),
-               None if below is None else below.data_ptr(), key.data_ptr(),
-               unreached.data_ptr() if count_unreached else None, sh)
+               None if below is None else below.data_ptr(), key.data_ptr(), None, sh)
         kk = key.clone()
         vert = LOW - (kk & LOW)
-        return kk, (kk >> 32) - 1, torch.where(kk > 0, vert, torch.full_like(vert, -1))
+        return kk, torch.where(kk > 0, vert, torch.full_like(vert, -1))
 
     # lowest-id member of every block: the deepest-vertex key of an all-unreached array
     level.fill_(-1)
-    sizes = torch.bincount(g.labels.to(torch.int64), minlength=k)
-    _, _, first = top(level)
-    bfs(first)
-    _, _, a = top(level, count_unreached=True)
-    disconnected = unreached > 0
-    bfs(a)
-    _, best, _ = top(level)
+    _, first = top(level)
+    _, a, reached = bfs(first, level)
+    disconnected = reached < sizes
+    lev_a = torch.empty_like(level)
+    best, _, _ = bfs(a, lev_a)
     # fringe refinement: the next deepest vertices of the second sweep, low id first
-    lev_a = level.clone()
     below = torch.full((k,), torch.iinfo(torch.int64).max, dtype=torch.int64, device="cuda")
     for _ in range(max(0, int(refinement_rounds))):
-        kr, _, root = top(lev_a, exclude=a, below=below)
+        kr, root = top(lev_a, exclude=a, below=below)
         if not bool((root >= 0).any().item()):
             break
         below = kr  # 0 where the block has no further vertex: nothing lies below it
-        bfs(root)
-        _, ecc, _ = top(level)
+        ecc, _, _ = bfs(root, level)
         best = torch.where(root >= 0, torch.maximum(best, ecc), best)
     out = best.to(torch.float64)
     out = torch.where(disconnected | (sizes == 0), torch.full_like(out, math.inf), out)

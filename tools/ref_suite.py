@@ -12,7 +12,11 @@ package's, exactly as the one-line shim at the end of `geopart/kmeans.py` would 
 * `test_acceptance.py`  -- ACCEPT-01..10 (`:108-231`: exact argmin, audit, convergence,
                            p-invariance), whose partitions now come from the GPU;
 * `test_estimators.py`  -- `GeographerPartitioner.fit` through the shim;
-* `test_cli.py`         -- `geopart partition --algo geographer` through the shim.
+* `test_cli.py`         -- `geopart partition --algo geographer` through the shim;
+* `test_fileio.py`, `test_metrics.py`, `test_graph.py` -- the formats and metrics either
+                           side of the path: the readers, the
+                           partition writer, the metrics and `GeometricGraph.validate`
+                           are replaced by the B200 ones (`integration.install_formats`).
 
 The test files are read from `--tests` (default: `/root/reference/pkg/tests` where it
 exists, else `baseline/_ref_tests`, the git-ignored copy `build()` makes so that it
@@ -33,7 +37,8 @@ import tempfile
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SUITE = ("test_kmeans.py", "test_acceptance.py", "test_estimators.py", "test_cli.py")
+SUITE = ("test_kmeans.py", "test_acceptance.py", "test_estimators.py", "test_cli.py",
+         "test_fileio.py", "test_metrics.py", "test_graph.py")
 
 
 def tests_dir(arg: str | None) -> str | None:
@@ -58,6 +63,7 @@ class Shim:
         from paper_1805_01208_b200 import integration
 
         integration.install(counter=self.calls)
+        integration.install_formats(counter=self.calls)
 
 
 def main(argv=None) -> int:
