@@ -218,51 +218,6 @@ def sample_ranks_device(n: int, seed: int, device, stream) -> torch.Tensor:
     return rank
 
 
-_early_pool = None
-
-
-def early_sample_ranks(points, settings, device):
-    """Start the warm-up permutation (kmeans.py:564-567) before the points are on the
-    device: it depends only on (n, seed), so for a host input it runs on a side stream
-    in a helper thread while the caller's thread stages the host -> device copy (the
-    permutation's kernels are bound by random HBM accesses, the copy by PCIe).  Returns
-    a future of the device ranks, or None when there is nothing to overlap.
-
-    Measured at C5 (2^30 points): pageable input 2.55 -> 2.40 s end to end.  A
-    page-locked input moves in one full-rate DMA, which the permutation's random HBM
-    traffic slows down by more than it saves (2.32 -> 2.40 s): not overlapped."""
-    global _early_pool
-    if isinstance(points, torch.Tensor) or os.environ.get("GP_EARLY_RANKS") == "0":
-        return None
-    shape = np.shape(points)
-    if len(shape) != 2 or shape[0] * shape[1] * 8 < (256 << 20):
-        return None
-    from . import staging
-
-    if isinstance(points, np.ndarray) and staging.is_pinned(points):
-        return None
-    n = int(shape[0])
-    if not sample_schedule(n, settings.init_sample) or settings.k > n:
-        return None
-    if _early_pool is None:
-        from concurrent.futures import ThreadPoolExecutor
-
-        _early_pool = ThreadPoolExecutor(1, thread_name_prefix="gp-early-ranks")
-
-    dev = torch.device(device)
-    index = torch.cuda.current_device() if dev.index is None else dev.index
-
-    def work():
-        torch.cuda.set_device(index)
-        side = torch.cuda.Stream(index)
-        with torch.cuda.stream(side):
-            rank = sample_ranks_device(n, settings.seed, dev, side.cuda_stream)
-        side.synchronize()
-        return rank
-
-    return _early_pool.submit(work)
-
-
 # warm-up samples with at most WALK_RATIO active points per center (and k >=
 # WALK_MIN_K) assign by warp-per-point grid walks instead of per-unit candidate
 # selection over the k centers (GP_WALK_RATIO=0 disables)
@@ -425,19 +380,6 @@ class DevicePartitioner:
 
     def _bootstrap(self, points, weights):
         st = self.settings
-        early = early_sample_ranks(points, st, self.device)
-        try:
-            return self._bootstrap_on_device(points, weights, early)
-        finally:
-            if early is not None and not early.done():
-                early.cancel()
-                try:
-                    early.result()
-                except BaseException:  # noqa: BLE001  (the primary error is propagating)
-                    pass
-
-    def _bootstrap_on_device(self, points, weights, early):
-        st = self.settings
         pts, w = self._input(points, weights)
         n, d = pts.shape
         self.n, self.d = n, d
@@ -491,11 +433,7 @@ class DevicePartitioner:
         # sample ranks in SFC order (kmeans.py:564-568)
         self.sizes = sample_schedule(n, st.init_sample)
         if self.sizes:
-            if early is not None:
-                rank_d = early.result()   # its stream was synchronised by the helper
-                rank_d.record_stream(torch.cuda.current_stream(dev))
-            else:
-                rank_d = sample_ranks_device(n, st.seed, dev, sh)
+            rank_d = sample_ranks_device(n, st.seed, dev, sh)
             self.rank_sfc = torch.empty(n, dtype=torch.int32, device=dev)
             N.call("gp_gather_ranks", rank_d.data_ptr(), self.gids.data_ptr(), n,
                    self.rank_sfc.data_ptr(), sh)
