@@ -299,7 +299,7 @@ __global__ void block_fold(const unsigned* __restrict__ order, const long long* 
 // block's frontier queue in global memory (a block's vertices enter it exactly once, so
 // block b owns queue[qbase[b], qbase[b + 1])), claims unvisited neighbors with an
 // atomicCAS on their level and synchronises its own levels with __syncthreads.
-constexpr int BFS_THREADS = 512;
+constexpr int BFS_THREADS = 256;   // frontiers are small; 8 CTAs per SM hide the per-level latency
 
 __global__ void __launch_bounds__(BFS_THREADS) bfs_blocks(
     const long long* __restrict__ off, const long long* __restrict__ nbr,
@@ -568,7 +568,7 @@ int gp_block_bfs(const int64_t* offsets, const int64_t* neighbors, const int32_t
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = k < sms * 4 ? k : sms * 4;
+  const int grid = k < sms * 8 ? k : sms * 8;
   bfs_blocks<<<grid, BFS_THREADS, 0, s>>>((const long long*)offsets, (const long long*)neighbors,
                                           assignment, k, (const long long*)roots,
                                           (const long long*)qbase, (long long*)queue, level,
