@@ -49,9 +49,9 @@ __host__ __device__ __forceinline__ bool is_break(unsigned c, unsigned next) {
   // '\n', or a '\r' that is not the first half of "\r\n" (universal newlines)
   return c == '\n' || (c == '\r' && next != '\n');
 }
-__host__ __device__ __forceinline__ bool is_space(unsigned c) {
-  return c == ' ' || c == '\t' || c == '\n' || c == '\r';
-}
+// blank: every byte <= ' ' (the host rejects a file holding control bytes other than
+// \t \n \r before any token is used, so those never separate tokens in practice)
+__host__ __device__ __forceinline__ bool is_space(unsigned c) { return c <= ' '; }
 
 // ---------------------------------------------------------------- number parsing
 __host__ __device__ inline unsigned long long mulhi64(unsigned long long a, unsigned long long b,
@@ -205,31 +205,51 @@ struct Chunk {
   unsigned brk, spc, hash, hi;  // break, whitespace, comment char, non-ASCII or control byte
 };
 
+// Word-wise byte tests: bit 7 of every byte of the result is set where the test holds.
+__device__ __forceinline__ unsigned bytes_ge(unsigned w, unsigned c) {   // byte >= c, c in 1..0x80
+  return (((w & 0x7f7f7f7fu) + (0x80u - c) * 0x01010101u) | w) & 0x80808080u;
+}
+__device__ __forceinline__ unsigned bytes_eq(unsigned w, unsigned c) {   // byte == c, c < 0x80
+  const unsigned x = w ^ (c * 0x01010101u);
+  return ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
+}
+// bits 7, 15, 23, 31 -> bits 0..3 (the four partial products do not overlap)
+__device__ __forceinline__ unsigned pack4(unsigned m) { return ((m >> 7) * 0x01020408u) >> 24; }
+
 __device__ __forceinline__ Chunk load_chunk(const unsigned char* __restrict__ text, long long len,
                                             long long base, int cmt_char) {
   Chunk c{0u, 0u, 0u, 0u};
-  unsigned char b[PER + 1];
   if (base + PER + 1 <= len && ((uintptr_t)(text + base) & 15) == 0) {
+    // four bytes per operation: classify each 32-bit word, pack the per-byte flags
     const uint4* p = reinterpret_cast<const uint4*>(text + base);
+    unsigned nl = 0, cr = 0;
 #pragma unroll
     for (int v = 0; v < PER / 16; ++v) {
       const uint4 x = p[v];
       const unsigned wds[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int m = 0; m < 4; ++m) b[v * 16 + k * 4 + m] = (unsigned char)(wds[k] >> (8 * m));
+      for (int k = 0; k < 4; ++k) {
+        const unsigned w = wds[k];
+        const int sh = 16 * v + 4 * k;
+        const unsigned e_nl = bytes_eq(w, '\n'), e_cr = bytes_eq(w, '\r');
+        const unsigned ctl = (bytes_ge(w, 0x20) ^ 0x80808080u) & ~(e_nl | e_cr | bytes_eq(w, '\t'));
+        c.spc |= pack4(bytes_ge(w, 0x21) ^ 0x80808080u) << sh;
+        nl |= pack4(e_nl) << sh;
+        cr |= pack4(e_cr) << sh;
+        c.hi |= pack4(bytes_ge(w, 0x7f) | ctl) << sh;
+        if (cmt_char) c.hash |= pack4(bytes_eq(w, (unsigned)cmt_char)) << sh;
+      }
     }
-    b[PER] = text[base + PER];
-  } else {
-#pragma unroll
-    for (int j = 0; j <= PER; ++j) b[j] = base + j < len ? text[base + j] : (unsigned char)'\n';
+    // a '\r' directly before a '\n' is not a break of its own
+    const unsigned next_nl = (nl >> 1) | (text[base + PER] == '\n' ? 0x80000000u : 0u);
+    c.brk = nl | (cr & ~next_nl);
+    return c;
   }
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
+#pragma unroll 1
+  for (int j = 0; j < PER; ++j) {   // the last chunks of the text
     if (base + j >= len) { c.spc |= 1u << j; continue; }  // past the end: padding
-    const unsigned ch = b[j];
-    const unsigned nx = base + j + 1 < len ? b[j + 1] : 0u;
+    const unsigned ch = text[base + j];
+    const unsigned nx = base + j + 1 < len ? text[base + j + 1] : 0u;
     if (is_break(ch, nx)) c.brk |= 1u << j;
     if (is_space(ch)) c.spc |= 1u << j;
     if (cmt_char && ch == (unsigned)cmt_char) c.hash |= 1u << j;
@@ -240,6 +260,8 @@ __device__ __forceinline__ Chunk load_chunk(const unsigned char* __restrict__ te
 
 // bits of the chunk that lie inside a '#' comment, given the state at its first byte
 __device__ __forceinline__ unsigned comment_mask(const Chunk& c, bool entering) {
+  if (!c.hash)   // no comment starts here: an entering one runs up to the first break
+    return !entering ? 0u : (c.brk ? (c.brk & (0u - c.brk)) - 1u : 0xffffffffu);
   unsigned m = 0;
   bool in = entering;
 #pragma unroll
@@ -446,10 +468,17 @@ __global__ void __launch_bounds__(TPB) text_emit(const unsigned char* __restrict
     if (ts >> j & 1u) {
       const unsigned char* t = text + base + j;
       const long long left = len - (base + j);
-      int tl = 0;
-      while (tl < left && tl <= MAX_TOKEN && !is_space(t[tl]) &&
-             !(cmt_char && t[tl] == (unsigned char)cmt_char))
-        ++tl;
+      // the token ends at the next blank or comment byte: inside this chunk by the masks
+      const unsigned rest = (c.spc | cmt) >> j;
+      int tl;
+      if (rest) {
+        tl = __ffs(rest) - 1;
+      } else {
+        tl = PER - j;
+        while (tl < left && tl <= MAX_TOKEN && !is_space(t[tl]) &&
+               !(cmt_char && t[tl] == (unsigned char)cmt_char))
+          ++tl;
+      }
       long long v;
       const int kind = parse_number(t, tl, &v);
       tok_val[t_id] = v;

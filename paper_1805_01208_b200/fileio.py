@@ -49,7 +49,12 @@ class MetisParseError(ValueError):
 def _read_bytes(source) -> np.ndarray:
     """The raw bytes of a path, text stream or byte stream (fileio.py:35-53)."""
     if isinstance(source, (str, Path)):
-        return np.fromfile(os.fspath(source), dtype=np.uint8)
+        path = os.fspath(source)
+        if os.path.getsize(path) >= (64 << 20):
+            # large files: map the page cache; the staging ring's host threads copy it
+            # straight into pinned chunks (no intermediate buffer)
+            return np.memmap(path, dtype=np.uint8, mode="r")
+        return np.fromfile(path, dtype=np.uint8)
     data = source.read()
     if isinstance(data, str):
         data = data.encode("ascii")
