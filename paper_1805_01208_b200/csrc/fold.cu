@@ -18,7 +18,6 @@
 //              by all lanes of the chunk;
 //   combine  : per block, fold the pair partials in segment order.
 #include <cub/block/block_scan.cuh>
-#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -27,6 +26,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "radix.cuh"
 
 namespace gp {
 
@@ -70,9 +70,7 @@ static FoldLayout layout(int64_t n_local, int64_t pos0, int64_t n_global, int k)
   cub::DeviceSelect::Flagged(nullptr, b1, cub::CountingInputIterator<int32_t>(0),
                              (const uint8_t*)nullptr, (int32_t*)nullptr, (int64_t*)nullptr,
                              (int)L.cap);
-  cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr);
-  cub::DoubleBuffer<int32_t> vb(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, b2, kb, vb, (int)L.cap, 0, 32);
+  b2 = radix::workspace_bytes(L.cap, 4, 4);   // the run sort's scratch (hand-written, radix.cu)
   L.cub_bytes = b1 > b2 ? b1 : b2;
   if (b3 > L.cub_bytes) L.cub_bytes = b3;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -796,20 +794,14 @@ int gp_movement_fold(const gp_fold_args* f, void* stream) {
     int64_t R = 0;
     GP_CUDA(cudaMemcpyAsync(&R, counters, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     GP_CUDA(cudaStreamSynchronize(s));
-    // stable LSD radix sort with ping-pong buffers (no n-sized CUB scratch)
-    cub::DoubleBuffer<uint32_t> kb(rkey, skey);
-    cub::DoubleBuffer<int32_t> vb(ridx, sidx);
-    size_t b = L.cub_bytes;
     // stable sort by the block bits only: valid blocks are < k < 2^bb - 1 and the
-    // invalid key is all-ones there, so the invalid runs stay last
-    GP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, b, kb, vb, (int)R, 0, block_bits(f->k), s));
-    skey = kb.Current();
-    sidx = vb.Current();
-    if (skey != (uint32_t*)(ws + L.off_skey_final)) {
-      // keep the sorted keys where gp_fold_export expects them
-      GP_CUDA(cudaMemcpyAsync(ws + L.off_skey_final, skey, R * sizeof(uint32_t),
-                              cudaMemcpyDeviceToDevice, s));
-      skey = (uint32_t*)(ws + L.off_skey_final);
+    // invalid key is all-ones there, so the invalid runs stay last (hand-written onesweep
+    // LSD passes, radix.cu; the sorted keys land where gp_fold_export expects them)
+    size_t b = L.cub_bytes;
+    if (R > 0) {
+      const int rc = radix::sort_pairs<uint32_t, int32_t>(rkey, ridx, skey, sidx, R, 0,
+                                                          block_bits(f->k), cub_tmp, b, s, false);
+      if (rc) return rc;
     }
     fold_pair_flags<<<grid_for(R, 256, sms * 16), 256, 0, s>>>(skey, R, counters, flags);
     b = L.cub_bytes;

@@ -3,7 +3,6 @@
 //
 // Reference semantics: geometry.py:112-192 (cells + Hilbert keys),
 // ranksim.py:143-170 (global sort + redistribution), kmeans.py:546-568.
-#include <cub/device/device_radix_sort.cuh>
 
 #include <cstdarg>
 #include <cstdio>
@@ -737,14 +736,7 @@ __global__ void cell_starts_kernel(const uint64_t* __restrict__ skeys, int k, in
 
 extern "C" int gp_center_grid_workspace_bytes(int k, size_t* bytes) {
   GP_REQUIRE(k >= 1, "gp_center_grid: k must be >= 1");
-  size_t b = 0;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint64_t*)nullptr,
-                                                  (uint64_t*)nullptr, (const uint32_t*)nullptr,
-                                                  (uint32_t*)nullptr, k, 0, 64);
-  if (e != cudaSuccess) {
-    gp::set_error("center grid workspace query failed: %s", cudaGetErrorString(e));
-    return GP_ERR_CUDA;
-  }
+  const size_t b = gp::radix::workspace_bytes(k, 8, 4);
   *bytes = 2 * (size_t)k * (sizeof(uint64_t) + sizeof(uint32_t)) + ((b + 255) & ~(size_t)255) + 256;
   return GP_OK;
 }
@@ -776,8 +768,9 @@ extern "C" int gp_center_grid(const double* centers, int k, int d, const double*
   else
     gp::center_cells_kernel<3><<<(k + 255) / 256, 256, 0, s>>>(centers, k, lo[0], lo[1], lo[2],
                                                                 h, G, kin, vin);
-  GP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, (uint32_t*)items, k, 0, bits,
-                                          s));
+  rc = gp::radix::sort_pairs<uint64_t, uint32_t>(kin, vin, kout, (uint32_t*)items, k, 0, bits, tmp,
+                                                 tb, s, false);
+  if (rc) return rc;
   gp::cell_starts_kernel<<<(unsigned)((ncell + 1 + 255) / 256), 256, 0, s>>>(kout, k, ncell,
                                                                              start);
   return gp::check_launch("center_grid");
