@@ -188,6 +188,37 @@ def test_larger_graphs_against_the_oracle(api, n, weights):
         assert rep.block_diameters == want["block_diameters"]
 
 
+def test_high_degree_vertices(api):
+    """Hubs above the per-thread neighbor limit take the warp-per-vertex volume path."""
+    from paper_1805_01208_b200.types import Partition
+
+    n = 4000
+    rng = np.random.default_rng(21)
+    ring = np.stack([np.arange(n), (np.arange(n) + 1) % n], 1)
+    hubs = []
+    for h, deg in ((0, 3000), (7, 49), (8, 48), (1234, 700)):
+        others = rng.choice(np.setdiff1d(np.arange(n), [h, (h - 1) % n, (h + 1) % n]), deg,
+                            replace=False)
+        hubs.append(np.stack([np.full(deg, h), others], 1))
+    e = np.concatenate([ring] + hubs)
+    e = np.unique(np.sort(e, axis=1), axis=0)
+    _, off, nb = G.csr_from_edges(n, e)
+    g = api.graph.GeometricGraph(off, nb, rng.random((n, 2)), np.ones(n))
+    g.validate()
+    for k in (3, 40, 500):
+        lab = rng.integers(0, k, n)
+        part = Partition(assignment=lab, k=k)
+        cmax, ctot, per = api.metrics.comm_volumes(g, part)
+        wmax, wtot, wper = O.comm_volumes(off, nb, lab, k)
+        assert (cmax, ctot) == (wmax, wtot) and np.array_equal(per, wper), k
+        assert api.metrics.edge_cut(g, part) == O.edge_cut(off, nb, None, lab)
+        assert np.array_equal(api.metrics.block_diameter_lower_bounds(g, part),
+                              O.diameters(off, nb, lab, k)), k
+    text = G.metis_text(n, off, nb)
+    back = api.fileio.load_metis_graph(io.StringIO(text))
+    assert G.same_bits(back.neighbors, nb) and G.same_bits(back.offsets, off)
+
+
 def test_injected_errors_match_the_oracle(api):
     n, off, nb, pts = G.random_geometric(30000, seed=11)
     base = G.metis_text(n, off, nb).split("\n")
