@@ -188,6 +188,56 @@ def test_larger_graphs_against_the_oracle(api, n, weights):
         assert rep.block_diameters == want["block_diameters"]
 
 
+def test_tokenizer_carries_across_chunk_and_tile_boundaries(api):
+    """Comments, CRLF pairs and tokens placed across the tokenizer's 32-byte thread chunks
+    and 8 KiB tiles (the comment carry, the '\\r' look-ahead and the token scan all cross
+    them), against np.loadtxt on the same text."""
+    import warnings
+
+    rng = np.random.default_rng(13)
+    TILE = 8192
+    for trial in range(6):
+        parts, size, rows = [], 0, 0
+        while size < 5 * TILE + 1000:
+            kind = rng.integers(0, 6)
+            if kind == 0:      # a long comment, likely to straddle a boundary
+                line = "#" + "c # 1 2 3 " * int(rng.integers(1, 200))
+            elif kind == 1:    # blank line with blanks and tabs
+                line = " \t" * int(rng.integers(0, 40))
+            else:              # a data row, values of very different lengths
+                a = rng.standard_normal() * 10.0 ** int(rng.integers(-30, 30))
+                b = int(rng.integers(-10 ** 9, 10 ** 9))
+                line = (" " * int(rng.integers(0, 30))) + ("%.17g" % a) + \
+                    ("\t" * int(rng.integers(1, 4))) + str(b) + \
+                    ("  # trailing " + "x" * int(rng.integers(0, 120)) if kind == 2 else "")
+                rows += 1
+            # pad so that interesting bytes land on tile / chunk boundaries now and then
+            if rng.integers(0, 4) == 0 and kind != 1:
+                room = (-(size + len(line)) - int(rng.integers(0, 3))) % 32
+                line += " " * room
+            eol = ("\r\n", "\n", "\r\n", "\n")[trial % 4] if trial < 4 else \
+                ("\r\n" if rng.integers(0, 2) else "\n")
+            parts.append(line + eol)
+            size += len(parts[-1])
+        text = "".join(parts)
+        if trial % 2:
+            text = text.rstrip("\r\n")   # no final newline
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            # universal newlines, as a file opened by path
+            want = np.loadtxt(io.StringIO(text.replace("\r\n", "\n")), dtype=np.float64, ndmin=2)
+        got = api.fileio.load_coords(io.BytesIO(text.encode()))
+        assert want.shape == (rows, 2) and G.same_bits(got, want), trial
+    # a '\\r' as the last byte of a tile, its '\\n' the first byte of the next one
+    body = "".join("%d %d\r\n" % (i, i * i) for i in range(3000))
+    for shift in range(0, 12):
+        text = " " * shift + body
+        got = api.fileio.load_coords(io.BytesIO(text.encode()))
+        assert got.shape == (3000, 2) and got[-1, 1] == 2999.0 ** 2 and got[17, 0] == 17.0
+    g = api.fileio.load_metis_graph(io.BytesIO(("%% c\r\n3 2\r\n2\r\n1 3\r\n2" ).encode()))
+    assert g.neighbors.tolist() == [1, 0, 2, 1]
+
+
 def test_high_degree_vertices(api):
     """Hubs above the per-thread neighbor limit take the warp-per-vertex volume path."""
     from paper_1805_01208_b200.types import Partition
