@@ -146,9 +146,10 @@ __host__ __device__ inline int parse_number(const unsigned char* t, int len, lon
   if (i == len) {  // integer grammar
     if (int_digits == 0) return GP_TOK_SUSPECT;
     if (sig <= 18) { *val = neg ? -(long long)w : (long long)w; return GP_TOK_INT; }
-    return GP_TOK_SUSPECT;
+    // 19 digits or more: not an int64 this parser vouches for; as a real it is
+    // converted below (an integer role then sends the token to the host)
   }
-  if (t[i] == '.') {
+  if (i < len && t[i] == '.') {
     ++i;
     while (i < len && t[i] >= '0' && t[i] <= '9') {
       const unsigned d = t[i] - '0';
@@ -173,9 +174,15 @@ __host__ __device__ inline int parse_number(const unsigned char* t, int len, lon
     }
     q += eneg ? -e : e;
   }
-  if (i != len || dropped) return GP_TOK_SUSPECT;  // trailing junk, or > 19 digits
+  if (i != len) return GP_TOK_SUSPECT;  // trailing junk
   unsigned long long bits;
   if (!decimal_to_double(w, q, neg, &bits)) return GP_TOK_SUSPECT;
+  if (dropped) {
+    // more than 19 significant digits: the value lies strictly between w and w + 1 units
+    // of 10^q; when both round to the same double, so does the value
+    unsigned long long above;
+    if (!decimal_to_double(w + 1, q, neg, &above) || above != bits) return GP_TOK_SUSPECT;
+  }
   *val = (long long)bits;
   return GP_TOK_REAL;
 }

@@ -83,8 +83,20 @@ class _Tokens:
     tok_kind: object          # device uint8 (n_tokens)
 
     def line_text(self, line: int) -> str:
-        lo, hi = (int(v) for v in self.line_off[line:line + 2].cpu().tolist())
-        return bytes(self.host[lo:hi]).decode("ascii").rstrip("\r\n")
+        return self.lines_text([line])[line]
+
+    def lines_text(self, lines) -> dict:
+        """{line: its text} for a batch of line numbers (one device read for all)."""
+        import torch
+
+        if not len(lines):
+            return {}
+        idx = torch.as_tensor(sorted(set(int(v) for v in lines)), dtype=torch.int64,
+                              device=self.line_off.device)
+        lo = self.line_off[idx].cpu().tolist()
+        hi = self.line_off[idx + 1].cpu().tolist()
+        return {int(l): bytes(self.host[a:b]).decode("ascii").rstrip("\r\n")
+                for l, a, b in zip(idx.cpu().tolist(), lo, hi)}
 
 
 def _tokenize(buf: np.ndarray, comment_char: int) -> _Tokens:
@@ -266,25 +278,34 @@ def load_metis_graph(graph_source, coord_source=None) -> GeometricGraph:
     if flagged.numel():
         # the host words the error of the first rejected line; a flagged line that Python
         # accepts (exotic but valid tokens) is patched with Python's values
-        patched = False
         lines = body_line[flagged].cpu().tolist()
-        for u, line in zip(flagged.cpu().tolist(), lines):
-            w, nb, ews = _vertex_line(tk.line_text(line), line + 1, u, n, has_vwgt, has_ewgt)
-            o0 = int(offsets[u].item())
-            if len(nb) != int(offsets[u + 1].item()) - o0:
+        texts = tk.lines_text(lines)
+        starts = offsets[flagged].cpu().tolist()
+        ends = offsets[flagged + 1].cpu().tolist()
+        p_pos, p_nb, p_ew, p_u, p_vw = [], [], [], [], []
+        for u, line, o0, o1 in zip(flagged.cpu().tolist(), lines, starts, ends):
+            w, nb, ews = _vertex_line(texts[line], line + 1, u, n, has_vwgt, has_ewgt)
+            if len(nb) != o1 - o0:
                 raise RuntimeError(f"line {line + 1}: tokenizer and host disagree on the degree")
-            if nb:
-                neighbors[o0:o0 + len(nb)] = torch.tensor(nb, dtype=torch.int64, device=dev)
-                if has_ewgt:
-                    ew[o0:o0 + len(nb)] = torch.tensor(ews, dtype=torch.float64, device=dev)
-            if has_vwgt:
-                vw[u] = w
-            patched = True
-        if patched:
-            flags.zero_()
-            chk, missing = structure()
-            if int(flags.sum().item()):
-                raise RuntimeError("structure check flags a line the host accepted")
+            p_pos.extend(range(o0, o1))
+            p_nb.extend(nb)
+            if has_ewgt:
+                p_ew.extend(ews)
+            p_u.append(u)
+            p_vw.append(w)
+        # every flagged line was accepted by Python: patch its values in
+        if p_pos:
+            pos = torch.tensor(p_pos, dtype=torch.int64, device=dev)
+            neighbors[pos] = torch.tensor(p_nb, dtype=torch.int64, device=dev)
+            if has_ewgt:
+                ew[pos] = torch.tensor(p_ew, dtype=torch.float64, device=dev)
+        if has_vwgt:
+            vw[torch.tensor(p_u, dtype=torch.int64, device=dev)] = \
+                torch.tensor(p_vw, dtype=torch.float64, device=dev)
+        flags.zero_()
+        chk, missing = structure()
+        if int(flags.sum().item()):
+            raise RuntimeError("structure check flags a line the host accepted")
 
     if nnz != 2 * m:
         raise MetisParseError(
@@ -339,23 +360,30 @@ def _table(source, want_int: bool, what: str):
     if bad_tok >= 0:
         # numpy's own converter decides every token outside the plain decimal grammar
         kinds = tk.tok_kind[:tk.n_tokens]
+        import warnings
+
         odd = torch.nonzero(kinds != TOK_INT if want_int else kinds > TOK_REAL).flatten()
         lines = (torch.searchsorted(tk.line_tok0, odd, right=True) - 1)
         col0 = (odd - tk.line_tok0[lines]).cpu().tolist()
-        for t, line, c in zip(odd.cpu().tolist(), lines.cpu().tolist(), col0):
-            tok = tk.line_text(line).split("#", 1)[0].split()[c]
+        lines = lines.cpu().tolist()
+        texts = {l: t.split("#", 1)[0].split() for l, t in tk.lines_text(lines).items()}
+        fixed_t, fixed_v = [], []
+        for t, line, c in zip(odd.cpu().tolist(), lines, col0):
+            tok = texts[line][c]
             try:
-                import warnings
-
                 with warnings.catch_warnings():
                     warnings.simplefilter("ignore")
                     val = np.loadtxt(io.StringIO(tok), dtype=np_dtype, ndmin=1, comments=None)
-                out[t] = val[0].item()
+                fixed_t.append(t)
+                fixed_v.append(val[0].item())
             except ValueError:
                 bad_line = line
                 bad_msg = (f"could not convert string {tok!r} to {dtype_name} at row "
                            f"{data_row(line)}, column {c + 1}.")
                 break
+        if fixed_t:
+            out[torch.tensor(fixed_t, dtype=torch.int64, device="cuda")] = \
+                torch.tensor(fixed_v, dtype=out.dtype, device="cuda")
     if ragged_line >= 0 and (bad_line is None or ragged_line <= bad_line):
         nt = int((tk.line_tok0[ragged_line + 1] - tk.line_tok0[ragged_line]).item())
         bad_msg = (f"the number of columns changed from {ncols} to {nt} at row "

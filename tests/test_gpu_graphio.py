@@ -238,6 +238,39 @@ def test_tokenizer_carries_across_chunk_and_tile_boundaries(api):
     assert g.neighbors.tolist() == [1, 0, 2, 1]
 
 
+def test_many_tokens_outside_the_plain_grammar(api):
+    """Thousands of tokens the device leaves to Python / numpy (the batched host path) and
+    long mantissas decided on the device: the arrays equal the oracle's."""
+    n, off, nb, pts = G.random_geometric(5000, seed=4)
+    rng = np.random.default_rng(9)
+    vw = rng.integers(1, 9, n).astype(np.float64)
+    lines = G.metis_text(n, off, nb, vw).split("\n")
+    for u in range(n):   # every vertex weight as +d, d_0 or 1e0-style: all valid for float()
+        t = lines[u + 1].split()
+        w = int(vw[u])
+        t[0] = (f"+{w}", f"{w}_0", f"{w}e0", f"{w}.000000000000000000000")[u % 4]
+        if u % 7 == 0 and len(t) > 1:
+            t[1] = "+" + t[1]     # int() accepts a sign
+        lines[u + 1] = " ".join(t)
+    text = "\n".join(lines)
+    want = O.parse_metis(text)
+    g = api.fileio.load_metis_graph(io.StringIO(text))
+    assert G.same_bits(g.offsets, want[0]) and G.same_bits(g.neighbors, want[1])
+    assert G.same_bits(g.vertex_weights, want[2])
+    ctext = "".join("%.25g %.30e\n" % (x, y) if i % 3 else "%.17g nan\n" % x
+                    for i, (x, y) in enumerate(pts))
+    with pytest.raises(api.fileio.MetisParseError, match="non-finite coordinate"):
+        api.fileio.load_coords(io.StringIO(ctext))
+    ctext = ctext.replace("nan", "1e400").replace("1e400", "0x", 1)
+    with pytest.raises(api.fileio.MetisParseError) as ei:
+        api.fileio.load_coords(io.StringIO(ctext))
+    with pytest.raises(O.ParseError) as eo:
+        O.coords_of(ctext)
+    assert str(ei.value) == str(eo.value)
+    ctext = "".join("%.25g %.30e\n" % (x, y) for x, y in pts)
+    assert G.same_bits(api.fileio.load_coords(io.StringIO(ctext)), O.coords_of(ctext))
+
+
 def test_high_degree_vertices(api):
     """Hubs above the per-thread neighbor limit take the warp-per-vertex volume path."""
     from paper_1805_01208_b200.types import Partition

@@ -120,7 +120,7 @@ def test_decimal_conversion_matches_python_float(parse_number):
         x = struct.unpack("<d", struct.pack("<Q", rng.getrandbits(64)))[0]
         if x != x or x in (float("inf"), float("-inf")):
             continue
-        for s in (repr(x), "%.17g" % x, "%.15g" % x, "%.10e" % x):
+        for s in (repr(x), "%.17g" % x, "%.15g" % x, "%.10e" % x, "%.25g" % x, "%.40e" % x):
             check(s)
     for i in range(60000):
         nd = rng.randint(1, 19)
@@ -136,8 +136,13 @@ def test_decimal_conversion_matches_python_float(parse_number):
               "2.2250738585072011e-308", "2.2250738585072014e-308", "1.7976931348623157e308",
               "1.7976931348623159e308", "1e-400", "1e400", "-0.0", ".5", "5.", "+.5e+1", "00012"):
         check(s)
-    assert suspects < checked // 10
-    for s in ("nan", "inf", "1_0", ".", "-", "1e", "1e+", "e5", "1.2.3", "0x10", "1,2",
-              "12345678901234567890", "1234567890123456789"):
+    for s in ("12345678901234567890", "1234567890123456789", "0.10000000000000000555",
+              "9007199254740993.00000000000000000001", "123456789012345678901234567890",
+              "9007199254740992.99999999999999999999"):
+        check(s)
+        assert parse_number(s)[0] in (1, 3), s    # never an int64 beyond 18 digits
+    assert parse_number("123456789012345678901234567890")[0] == 1
+    assert suspects < checked // 50   # long mantissas are decided by bracketing (w, w + 1)
+    for s in ("nan", "inf", "1_0", ".", "-", "1e", "1e+", "e5", "1.2.3", "0x10", "1,2"):
         assert parse_number(s)[0] == 3, s
     assert parse_number("%abc")[0] == 2
