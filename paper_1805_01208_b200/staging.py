@@ -31,7 +31,9 @@ def _threads() -> ThreadPoolExecutor:
             cores = len(os.sched_getaffinity(0))
         except AttributeError:
             cores = os.cpu_count() or 1
-        _pool = ThreadPoolExecutor(max(1, min(8, cores)))
+        # GP_STAGE_THREADS: host copy threads filling / draining the pinned ring
+        want = int(os.environ.get("GP_STAGE_THREADS", "8"))
+        _pool = ThreadPoolExecutor(max(1, min(want, cores)))
     return _pool
 
 
