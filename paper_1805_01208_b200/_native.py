@@ -158,7 +158,7 @@ def check(rc: int, what: str = "") -> None:
 # counted as one histogram pass plus one launch per 8-bit digit pass
 KERNELS_PER_CALL = {
     "gp_box_minmax": 2, "gp_weight_probe": 1, "gp_hilbert_keys": 1, "gp_sort_pairs": 9,
-    "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 4,
+    "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 1,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
     "gp_scatter_by_gid": 1, "gp_gather_ranks": 1,
     "gp_group_boxes": 1,

@@ -357,45 +357,108 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, int64_t ldx, in
 }
 
 // ------------------------------------------------------- K5 compaction
-// Ordered compaction of {i : rank[i] < size} in two passes over warp chunks of
-// CW = 512 consecutive entries (no block-wide barriers): per-chunk counts, a device
-// scan of the counts, then every warp writes its chunk's indices by ballot.
-constexpr int CW = 512;
+// Ordered compaction of {i : rank[i] < size} in ONE pass (rank is read once): persistent
+// CTAs take tiles of CT = 4096 consecutive entries in order from a ticket counter; a
+// tile's threads count their 16 consecutive entries, a block scan orders them, the tile's
+// place in the output comes from a decoupled look-back over the earlier tiles' published
+// counts (one 64-bit status word per tile: flag in the top two bits), and the selected
+// indices are staged in shared memory and written out as one contiguous run.
+constexpr int CTH = 256;            // threads per CTA
+constexpr int CPER = 16;            // consecutive entries per thread (32: 44 vs 31 ms at C5)
+constexpr int CT = CTH * CPER;      // entries per tile
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = ST_AGG - 1;
 
-__global__ void compact_count(const int32_t* __restrict__ rank, int64_t n, int64_t size,
-                              int64_t* __restrict__ counts, int64_t nch) {
-  const int lane = threadIdx.x & 31;
-  const int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (ch >= nch) return;
-  int c = 0;
+__global__ void __launch_bounds__(CTH) compact_onepass(const int32_t* __restrict__ rank, int64_t n,
+                                                       int64_t size, int64_t ntiles,
+                                                       unsigned long long* __restrict__ ticket,
+                                                       unsigned long long* __restrict__ status,
+                                                       int32_t* __restrict__ idx,
+                                                       int64_t* __restrict__ total) {
+  __shared__ int32_t s_out[CT];
+  __shared__ int s_warp[CTH / 32];
+  __shared__ long long s_tile, s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (;;) {
+    __syncthreads();   // the previous tile's staging buffer and cursors are free
+    if (tid == 0) s_tile = (long long)atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const long long tile = s_tile;
+    if (tile >= ntiles) return;
+    const long long e0 = tile * CT + (long long)tid * CPER;
+    // this thread's entries as a bit mask
+    unsigned sel = 0;
+    if (e0 + CPER <= n) {
+      const int4* p = reinterpret_cast<const int4*>(rank + e0);
 #pragma unroll
-  for (int r = 0; r < CW / 32; ++r) {
-    const int64_t i = ch * CW + r * 32 + lane;
-    c += (i < n && rank[i] < size);
-  }
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-  if (lane == 0) counts[ch] = c;
-}
-
-__global__ void compact_write(const int32_t* __restrict__ rank, int64_t n, int64_t size,
-                              const int64_t* __restrict__ offsets, int64_t nch,
-                              int32_t* __restrict__ idx, int64_t* __restrict__ total) {
-  const int lane = threadIdx.x & 31;
-  const int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (ch == 0 && lane == 0) *total = offsets[nch];
-  if (ch >= nch) return;
-  int64_t run = offsets[ch];
-  bool f[CW / 32];
+      for (int v = 0; v < CPER / 4; ++v) {
+        const int4 r = p[v];
+        sel |= (unsigned)(r.x < size) << (4 * v) | (unsigned)(r.y < size) << (4 * v + 1) |
+               (unsigned)(r.z < size) << (4 * v + 2) | (unsigned)(r.w < size) << (4 * v + 3);
+      }
+    } else {
+      for (int j = 0; j < CPER; ++j)
+        if (e0 + j < n && rank[e0 + j] < size) sel |= 1u << j;
+    }
+    const int mine = __popc(sel);
+    int incl = mine;
 #pragma unroll
-  for (int r = 0; r < CW / 32; ++r) {
-    const int64_t i = ch * CW + r * 32 + lane;
-    f[r] = i < n && rank[i] < size;
-  }
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int before = incl - mine, tile_count = 0;
 #pragma unroll
-  for (int r = 0; r < CW / 32; ++r) {
-    const unsigned b = __ballot_sync(FULL, f[r]);
-    if (f[r]) idx[run + __popc(b & ((1u << lane) - 1))] = (int32_t)(ch * CW + r * 32 + lane);
-    run += __popc(b);
+    for (int w2 = 0; w2 < CTH / 32; ++w2) {
+      if (w2 < warp) before += s_warp[w2];
+      tile_count += s_warp[w2];
+    }
+    // publish this tile's count, then look back for the tiles before it (warp 0)
+    if (warp == 0) {
+      if (lane == 0)
+        atomicExch(&status[tile], (tile == 0 ? ST_INC : ST_AGG) | (unsigned long long)tile_count);
+      long long base = 0;
+      if (tile > 0) {
+        long long t = tile - 1;
+        for (;;) {
+          // lanes look at 32 earlier tiles at once; the nearest inclusive prefix ends it
+          const long long tt = t - lane;
+          unsigned long long st = 0;
+          if (tt >= 0) {
+            do {
+              st = atomicAdd(&status[tt], 0ull);
+            } while (!(st >> 62));
+          } else {
+            st = ST_INC;   // before the first tile: an inclusive prefix of zero
+          }
+          const unsigned inc = __ballot_sync(FULL, (st >> 62) == 2);
+          const int stop = inc ? __ffs(inc) - 1 : 32;   // lanes 0..stop contribute
+          long long v = lane <= stop ? (long long)(st & ST_VAL) : 0;
+          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+          base += v;
+          if (inc) break;
+          t -= 32;
+        }
+        if (lane == 0)
+          atomicExch(&status[tile], ST_INC | (unsigned long long)(base + tile_count));
+      }
+      if (lane == 0) {
+        s_base = base;
+        if (tile == ntiles - 1) *total = base + tile_count;
+      }
+    }
+    // stage the selected indices in entry order, then one contiguous copy
+    int o = before;
+    unsigned m = sel;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      s_out[o++] = (int32_t)(e0 + j);
+    }
+    __syncthreads();
+    const long long base = s_base;
+    for (int i = tid; i < tile_count; i += CTH) idx[base + i] = s_out[i];
   }
 }
 
@@ -624,38 +687,33 @@ int gp_gather_rows(const double* X, int64_t ldx, int d, const int64_t* positions
   return check_launch("gather_rows");
 }
 
-static size_t compact_scan_bytes(int64_t nch) {
-  size_t b = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int64_t*)nullptr, (int64_t*)nullptr,
-                                (int)nch + 1);
-  return b;
-}
-
 int gp_compact_workspace_bytes(int64_t n, size_t* bytes) {
-  const int64_t nch = (n + CW - 1) / CW;
-  *bytes = ((size_t)(nch + 1) * sizeof(int64_t) + 255) / 256 * 256 + compact_scan_bytes(nch);
+  const int64_t nt = (n + CT - 1) / CT;
+  *bytes = 256 + ((size_t)(nt + 1) * sizeof(unsigned long long) + 255) / 256 * 256;
   return GP_OK;
 }
 
 int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx, int64_t* count,
                       void* workspace, size_t workspace_bytes, void* stream) {
-  const int64_t nch = (n + CW - 1) / CW;
   size_t need = 0;
   gp_compact_workspace_bytes(n, &need);
   GP_REQUIRE(workspace_bytes >= need, "gp_compact_active: workspace too small");
+  GP_REQUIRE(((uintptr_t)rank & 15) == 0, "gp_compact_active: rank must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
   if (n == 0) {
     GP_CUDA(cudaMemsetAsync(count, 0, sizeof(int64_t), s));
     return GP_OK;
   }
-  int64_t* counts = (int64_t*)workspace;
-  void* tmp = (char*)workspace + ((size_t)(nch + 1) * sizeof(int64_t) + 255) / 256 * 256;
-  const unsigned g = (unsigned)((nch * 32 + 255) / 256);
-  compact_count<<<g, 256, 0, s>>>(rank, n, size, counts, nch);
-  GP_CUDA(cudaMemsetAsync(counts + nch, 0, sizeof(int64_t), s));
-  size_t tb = compact_scan_bytes(nch);
-  GP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, counts, (int)nch + 1, s));
-  compact_write<<<g, 256, 0, s>>>(rank, n, size, counts, nch, idx, count);
+  const int64_t nt = (n + CT - 1) / CT;
+  GP_CUDA(cudaMemsetAsync(workspace, 0, need, s));   // ticket and every tile's status
+  unsigned long long* ticket = (unsigned long long*)workspace;
+  unsigned long long* status = (unsigned long long*)((char*)workspace + 256);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t cap = (int64_t)sms * 6;
+  compact_onepass<<<(unsigned)(nt < cap ? nt : cap), CTH, 0, s>>>(rank, n, size, nt, ticket, status,
+                                                                 idx, count);
   return check_launch("compact_active");
 }
 
