@@ -271,11 +271,12 @@ class _Hierarchy:
         N.call("gp_group_boxes", eng.aargs.X, eng.ldx, d, list_ptr, m, self.SUPER_SHIFT,
                self.sbox.data_ptr(), eng.sh)
         if self.use_mega:
-            self.mbox = torch.empty(self.nm * 2 * d, dtype=torch.float64, device=dev)
             self.mlist = torch.empty(self.nm * self.MEGA_CAP, dtype=torch.int32, device=dev)
             self.mcount = torch.empty(self.nm, dtype=torch.int32, device=dev)
-            N.call("gp_group_boxes", eng.aargs.X, eng.ldx, d, list_ptr, m,
-                   self.MEGA_SHIFT, self.mbox.data_ptr(), eng.sh)
+            # mega boxes = unions of their 64 super boxes (min / max are exact: the same
+            # boxes as a second pass over the points, without reading them again)
+            self.mbox = self._unions(self.sbox, self.ns, self.MEGA_SHIFT - self.SUPER_SHIFT,
+                                     self.nm, d)
         # a third level (2^24 entries) when there are many mega groups: the mega
         # lists then start from a giga list instead of all k
         self.use_giga = self.use_mega and m > (1 << (self.GIGA_SHIFT + 1))
@@ -283,20 +284,27 @@ class _Hierarchy:
             self.ng = (m + (1 << self.GIGA_SHIFT) - 1) >> self.GIGA_SHIFT
             self.glist = torch.empty(self.ng * self.GIGA_CAP, dtype=torch.int32, device=dev)
             self.gcount = torch.empty(self.ng, dtype=torch.int32, device=dev)
-            # giga boxes = unions of their 16 mega boxes (empty boxes are +inf/-inf)
-            r = 1 << (self.GIGA_SHIFT - self.MEGA_SHIFT)
-            mb = self.mbox.view(self.nm, 2, d)
-            pad = self.ng * r - self.nm
-            if pad:
-                fill = torch.empty((pad, 2, d), dtype=torch.float64, device=dev)
-                fill[:, 0], fill[:, 1] = math.inf, -math.inf
-                mb = torch.cat([mb, fill])
-            mb = mb.view(self.ng, r, 2, d)
-            self.gbox = torch.stack([mb[:, :, 0].amin(dim=1), mb[:, :, 1].amax(dim=1)],
-                                    dim=1).contiguous().view(-1)
+            # giga boxes = unions of their 16 mega boxes
+            self.gbox = self._unions(self.mbox, self.nm, self.GIGA_SHIFT - self.MEGA_SHIFT,
+                                     self.ng, d)
         a = eng.aargs
         a.group_list, a.group_count = self.slist.data_ptr(), self.scount.data_ptr()
         a.group_cap, a.group_shift = self.SUPER_CAP, self.SUPER_SHIFT
+
+    @staticmethod
+    def _unions(child, n_child, ratio_log2, n_parent, d):
+        """Boxes of groups made of 2^ratio_log2 consecutive child groups (k-sized torch
+        reductions; a missing child is the empty box +inf / -inf)."""
+        r = 1 << ratio_log2
+        cb = child.view(n_child, 2, d)
+        pad = n_parent * r - n_child
+        if pad:
+            fill = torch.empty((pad, 2, d), dtype=torch.float64, device=child.device)
+            fill[:, 0], fill[:, 1] = math.inf, -math.inf
+            cb = torch.cat([cb, fill])
+        cb = cb.view(n_parent, r, 2, d)
+        return torch.stack([cb[:, :, 0].amin(dim=1), cb[:, :, 1].amax(dim=1)],
+                           dim=1).contiguous().view(-1)
 
     def refresh(self):
         """Candidate lists under the current centers and influences (every round)."""
