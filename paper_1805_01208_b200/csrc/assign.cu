@@ -1346,10 +1346,28 @@ __global__ void __launch_bounds__(256) group_candidates_warp_kernel(
       nsrc = pc;
     }
   }
+  // four candidates per lane and step: their list entries, centers and 1/infl^2 bounds are
+  // loaded together (the loop is bound by the latency of these dependent loads)
+  constexpr int UN = 4;
   double m1 = INFINITY, m2 = INFINITY;
-  for (int i = lane; i < nsrc; i += 32) {
-    const int c = src ? src[i] : i;
-    two_min_merge(m1, m2, box_usq<D>(centers + c * D, lo, hi, inv2_hi[c]), INFINITY);
+  for (int b = 0; b < nsrc; b += 32 * UN) {
+    int c[UN];
+    double cen[UN][D], iv[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int i = b + 32 * u + lane;
+      c[u] = i < nsrc ? (src ? src[i] : i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int cc = c[u] < 0 ? 0 : c[u];
+#pragma unroll
+      for (int j = 0; j < D; ++j) cen[u][j] = centers[cc * D + j];
+      iv[u] = inv2_hi[cc];
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u)
+      if (c[u] >= 0) two_min_merge(m1, m2, box_usq<D>(cen[u], lo, hi, iv[u]), INFINITY);
   }
   for (int o = 16; o; o >>= 1) {
     const double b1 = __shfl_xor_sync(FULL, m1, o);
@@ -1359,18 +1377,29 @@ __global__ void __launch_bounds__(256) group_candidates_warp_kernel(
   const double U = m2;
   int32_t* out = list + g * (int64_t)cap;
   int n = 0;
-  for (int b = 0; b < nsrc; b += 32) {
-    const int i = b + lane;
-    bool take = false;
-    int c = 0;
-    if (i < nsrc) {
-      c = src ? src[i] : i;
-      take = box_lsq<D>(centers + c * D, lo, hi, inv2_lo[c]) <= U;
+  for (int b = 0; b < nsrc; b += 32 * UN) {
+    int c[UN];
+    double cen[UN][D], iv[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int i = b + 32 * u + lane;
+      c[u] = i < nsrc ? (src ? src[i] : i) : -1;
     }
-    const unsigned bal = __ballot_sync(FULL, take);
-    const int slot = n + __popc(bal & ((1u << lane) - 1));
-    if (take && slot < cap) out[slot] = c;
-    n += __popc(bal);
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int cc = c[u] < 0 ? 0 : c[u];
+#pragma unroll
+      for (int j = 0; j < D; ++j) cen[u][j] = centers[cc * D + j];
+      iv[u] = inv2_lo[cc];
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {   // entry order: sub-step u, then lane
+      const bool take = c[u] >= 0 && box_lsq<D>(cen[u], lo, hi, iv[u]) <= U;
+      const unsigned bal = __ballot_sync(FULL, take);
+      const int slot = n + __popc(bal & ((1u << lane) - 1));
+      if (take && slot < cap) out[slot] = c[u];
+      n += __popc(bal);
+    }
   }
   if (lane == 0) count[g] = n <= cap ? n : -1;
 }
