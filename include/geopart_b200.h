@@ -345,6 +345,13 @@ int gp_audit(const gp_assign_args* args, unsigned long long* out, void* stream);
 /* K9  result delivery: out[gids[i]] = a[i] (kmeans.py:637-641). */
 int gp_scatter_by_gid(const int32_t* a, const uint32_t* gids, int64_t n, int64_t* out,
                       void* stream);
+/* The same delivery when gids is a permutation of 0..n-1 (one shard holding every point),
+ * without random writes: two radix passes on the high gid bits group the (gid, block)
+ * pairs into windows of 2^14 consecutive ids, then one CTA per window places its pairs in
+ * shared memory and writes the window's labels as one contiguous run. */
+int gp_deliver_workspace_bytes(int64_t n, size_t* bytes);
+int gp_deliver_permutation(const int32_t* a, const uint32_t* gids, int64_t n, int64_t* out,
+                           void* workspace, size_t workspace_bytes, void* stream);
 
 /* Sample-rank delivery in SFC order: out[i] = rank_by_gid[gids[i]]
  * (kmeans.py:568). */

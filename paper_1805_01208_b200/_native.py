@@ -90,6 +90,8 @@ _SIGS = {
     "gp_fold_combine": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, sz,
                                   vp]),
     "gp_scatter_by_gid": (C.c_int, [vp, vp, i64, vp, vp]),
+    "gp_deliver_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
+    "gp_deliver_permutation": (C.c_int, [vp, vp, i64, vp, vp, sz, vp]),
     "gp_gather_state": (C.c_int, [vp, i64, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp,
                                   vp]),
     "gp_scatter_state": (C.c_int, [vp, i64, vp, vp, vp, vp, vp]),
@@ -160,7 +162,7 @@ KERNELS_PER_CALL = {
     "gp_box_minmax": 2, "gp_weight_probe": 1, "gp_hilbert_keys": 1, "gp_sort_pairs": 9,
     "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 1,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
-    "gp_scatter_by_gid": 1, "gp_gather_ranks": 1,
+    "gp_scatter_by_gid": 1, "gp_deliver_permutation": 4, "gp_gather_ranks": 1,
     "gp_group_boxes": 1,
     "gp_group_candidates": 1, "gp_sample_ranks": 170, "gp_gather_state": 1, "gp_scatter_state": 1, "gp_update_maps": 3, "gp_region_maps": 1, "gp_lb_remap": 1, "gp_fold_export": 1, "gp_fold_combine": 3,
     "gp_sfc_cut": 3, "gp_predict": 1, "gp_balance_decide": 1, "gp_center_grid": 3,

@@ -469,6 +469,21 @@ __global__ void scatter_gid_kernel(const int32_t* __restrict__ a, const uint32_t
     out[g[i]] = a[i];
 }
 
+// labels of one window of 2^DW_SHIFT consecutive ids: the window's pairs (grouped by the
+// radix passes on the high id bits) are placed by id in shared memory, then written out
+constexpr int DW_SHIFT = 14, DW = 1 << DW_SHIFT;
+__global__ void __launch_bounds__(512) deliver_window_kernel(const uint32_t* __restrict__ g,
+                                                             const int32_t* __restrict__ a,
+                                                             int64_t n, int64_t* __restrict__ out) {
+  extern __shared__ int32_t s_lab[];
+  const int64_t w0 = (int64_t)blockIdx.x << DW_SHIFT;
+  const int cnt = (int)(n - w0 < DW ? n - w0 : DW);
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+    s_lab[g[w0 + i] & (DW - 1)] = a[w0 + i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) out[w0 + i] = s_lab[i];
+}
+
 __global__ void gather_ranks_kernel(const int32_t* __restrict__ r, const uint32_t* __restrict__ g,
                                     int64_t n, int32_t* __restrict__ out) {
   constexpr int U = 4;
@@ -742,6 +757,41 @@ int gp_scatter_by_gid(const int32_t* a, const uint32_t* gids, int64_t n, int64_t
   if (n == 0) return GP_OK;
   scatter_gid_kernel<<<stride_grid(n), 256, 0, (cudaStream_t)stream>>>(a, gids, n, out);
   return check_launch("scatter_by_gid");
+}
+
+int gp_deliver_workspace_bytes(int64_t n, size_t* bytes) {
+  GP_REQUIRE(n >= 0 && n < (1ll << 31), "gp_deliver: n out of range");
+  *bytes = 2 * (((size_t)n * 4 + 255) & ~(size_t)255) + radix::workspace_bytes(n, 4, 4);
+  return GP_OK;
+}
+
+int gp_deliver_permutation(const int32_t* a, const uint32_t* gids, int64_t n, int64_t* out,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (n == 0) return GP_OK;
+  int bits = 1;
+  while (bits < 32 && ((uint64_t)(n - 1) >> bits) != 0) ++bits;
+  if (bits <= DW_SHIFT)   // one window: the plain scatter stays inside shared-memory reach
+    return gp_scatter_by_gid(a, gids, n, out, stream);
+  size_t need = 0;
+  gp_deliver_workspace_bytes(n, &need);
+  GP_REQUIRE(workspace_bytes >= need, "gp_deliver_permutation: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t arr = ((size_t)n * 4 + 255) & ~(size_t)255;
+  uint32_t* gs = (uint32_t*)workspace;
+  int32_t* as = (int32_t*)((char*)workspace + arr);
+  void* rws = (char*)workspace + 2 * arr;
+  int rc = radix::sort_pairs<uint32_t, int32_t>(gids, a, gs, as, n, DW_SHIFT, bits, rws,
+                                                workspace_bytes - 2 * arr, s, false);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(deliver_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DW * (int)sizeof(int32_t));
+    attr = true;
+  }
+  const int64_t nw = (n + DW - 1) >> DW_SHIFT;
+  deliver_window_kernel<<<(unsigned)nw, 512, DW * sizeof(int32_t), s>>>(gs, as, n, out);
+  return check_launch("deliver_permutation");
 }
 
 int gp_gather_ranks(const int32_t* rank_by_gid, const uint32_t* gids, int64_t n, int32_t* out,

@@ -1036,8 +1036,16 @@ class DevicePartitioner:
 
     def _deliver_ids(self, A):
         out = torch.empty(self.n, dtype=torch.int64, device=self.device)
-        N.call("gp_scatter_by_gid", A.data_ptr(), self.gids.data_ptr(), self.n, out.data_ptr(),
-               self.sh)
+        # one shard: the gids are a permutation of 0..n-1, delivered without random writes
+        # (radix-grouped windows); the sort scratch reuses the buffers the run is done with
+        for name in ("UBLB", "A_d", "UBLB_d", "X_d", "W_d", "rank_sfc", "active_idx", "assign_ws",
+                     "fold_ws"):
+            if hasattr(self, name):
+                setattr(self, name, None)
+        wsb = N.size_query("gp_deliver_workspace_bytes", self.n)
+        ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=self.device)
+        N.call("gp_deliver_permutation", A.data_ptr(), self.gids.data_ptr(), self.n,
+               out.data_ptr(), ws.data_ptr(), wsb, self.sh)
         return out
 
     def release(self):
