@@ -1281,10 +1281,28 @@ __global__ void __launch_bounds__(256) group_candidates_kernel(
       nsrc = pc;
     }
   }
+  // four candidates per thread and step: their list entries, centers and 1/infl^2 bounds
+  // are loaded together (the loops are bound by the latency of these dependent loads)
+  constexpr int UN = 4;
   double m1 = INFINITY, m2 = INFINITY;
-  for (int i = threadIdx.x; i < nsrc; i += blockDim.x) {
-    const int c = src ? src[i] : i;
-    two_min_merge(m1, m2, box_usq<D>(centers + c * D, lo, hi, inv2_hi[c]), INFINITY);
+  for (int b = 0; b < nsrc; b += (int)blockDim.x * UN) {
+    int c[UN];
+    double cen[UN][D], iv[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int i = b + (int)blockDim.x * u + (int)threadIdx.x;
+      c[u] = i < nsrc ? (src ? src[i] : i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int cc = c[u] < 0 ? 0 : c[u];
+#pragma unroll
+      for (int j = 0; j < D; ++j) cen[u][j] = centers[cc * D + j];
+      iv[u] = inv2_hi[cc];
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u)
+      if (c[u] >= 0) two_min_merge(m1, m2, box_usq<D>(cen[u], lo, hi, iv[u]), INFINITY);
   }
   for (int o = 16; o; o >>= 1) {
     const double b1 = __shfl_xor_sync(FULL, m1, o);
@@ -1301,12 +1319,27 @@ __global__ void __launch_bounds__(256) group_candidates_kernel(
   for (int w = 1; w < (int)(blockDim.x / 32); ++w) two_min_merge(m1, m2, s_two[0][w], s_two[1][w]);
   const double U = m2;
   int32_t* out = list + g * (int64_t)cap;
-  for (int i = threadIdx.x; i < nsrc; i += blockDim.x) {
-    const int c = src ? src[i] : i;
-    const double lsq = box_lsq<D>(centers + c * D, lo, hi, inv2_lo[c]);
-    if (lsq <= U) {
-      const int slot = atomicAdd(&s_n, 1);
-      if (slot < cap) out[slot] = c;
+  for (int b = 0; b < nsrc; b += (int)blockDim.x * UN) {
+    int c[UN];
+    double cen[UN][D], iv[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int i = b + (int)blockDim.x * u + (int)threadIdx.x;
+      c[u] = i < nsrc ? (src ? src[i] : i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int cc = c[u] < 0 ? 0 : c[u];
+#pragma unroll
+      for (int j = 0; j < D; ++j) cen[u][j] = centers[cc * D + j];
+      iv[u] = inv2_lo[cc];
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      if (c[u] >= 0 && box_lsq<D>(cen[u], lo, hi, iv[u]) <= U) {
+        const int slot = atomicAdd(&s_n, 1);
+        if (slot < cap) out[slot] = c[u];
+      }
     }
   }
   __syncthreads();
@@ -1789,8 +1822,10 @@ int gp_group_candidates(const double* boxes, int64_t ngroups, int d, int k,
   GP_REQUIRE(cap >= 1 && k >= 1, "gp_group_candidates: bad sizes");
   if (ngroups <= 0) return GP_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  // short parent lists (super groups under mega / giga lists): one warp per group
-  if (parent_list && parent_cap <= 4096) {
+  // short parent lists (super groups under mega / giga lists): one warp per group, when
+  // there are enough groups to fill the GPU with warps; a few hundred groups (warm-up
+  // samples) take a CTA each, so that the walk over the parent list is 8x shorter
+  if (parent_list && parent_cap <= 4096 && ngroups >= 4096) {
     const unsigned gw = (unsigned)((ngroups * 32 + 255) / 256);
     if (d == 2)
       group_candidates_warp_kernel<2><<<gw, 256, 0, s>>>(
