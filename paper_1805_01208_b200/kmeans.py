@@ -826,15 +826,19 @@ class DevicePartitioner:
                                           pin_memory=True)
             self.fold_h.copy_(self.fold_out, non_blocking=True)
             self.stream.synchronize()
-            red = self.fold_h.numpy().copy()
+            red = self.fold_h.numpy()   # read before the next fold overwrites it
             sums = red[:k * d].reshape(k, d)
             totals = red[k * d:k * (d + 1)]
             extents = red[k * (d + 1):k * (d + 2)]
             obj_parts = red[k * (d + 2):k * (d + 3)]
             empty = totals == 0
-            safe = np.where(empty, 1.0, totals)
-            new_centers = sums / safe[:, None]
-            new_centers[empty] = centers[empty]
+            any_empty = bool(empty.any())
+            if any_empty:
+                safe = np.where(empty, 1.0, totals)
+                new_centers = sums / safe[:, None]
+                new_centers[empty] = centers[empty]
+            else:   # the common case, same bits: no block lost all its points
+                new_centers = sums / totals[:, None]
             moves = row_norms(new_centers - centers)
             stats.iterations.append(IterationRecord(
                 phase=phase, active_points=self.m_global, balance_rounds=info.rounds,
@@ -847,10 +851,15 @@ class DevicePartitioner:
                 stats.converged = converged
                 break
             old_infl = infl
-            nxt = old_infl * np.where(empty, 1.0 + st.influence_step_cap, 1.0)
+            # (x * 1.0 is x: without empty blocks the influences enter the erosion as is)
+            nxt = old_infl * np.where(empty, 1.0 + st.influence_step_cap, 1.0) if any_empty \
+                else old_infl.copy()
             if st.erosion:
                 nonempty = block_w > 0
-                beta = float(2.0 * extents[nonempty].mean()) if nonempty.any() else 0.0
+                if nonempty.all():   # the mean of the same elements in the same order
+                    beta = float(2.0 * extents.mean())
+                else:
+                    beta = float(2.0 * extents[nonempty].mean()) if nonempty.any() else 0.0
                 if beta > 0:
                     nxt = eroded(nxt, moves, beta)
             centers = new_centers
