@@ -105,6 +105,13 @@ int gp_gather_rows(const double* X, int64_t ldx, int d, const int64_t* positions
 int gp_compact_workspace_bytes(int64_t n, size_t* bytes);
 int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx,
                       int64_t* count, void* workspace, size_t workspace_bytes, void* stream);
+/* The same over a candidate subset: idx <- positions[j] (increasing) with rank[j] < size,
+ * where (positions, rank) list the entries of a larger sample in position order (the
+ * warm-up sizes double, so small samples are compacted from a list of a few million
+ * candidates instead of all n ranks).  positions NULL: gp_compact_active. */
+int gp_compact_candidates(const int32_t* rank, const int32_t* positions, int64_t n, int64_t size,
+                          int32_t* idx, int64_t* count, void* workspace, size_t workspace_bytes,
+                          void* stream);
 
 /* Dense view of a sample phase's active entries (the ~20 balance rounds of one
  * movement iteration then stream contiguous arrays instead of gathering through

@@ -67,6 +67,7 @@ _SIGS = {
     "gp_gather_rows": (C.c_int, [vp, i64, C.c_int, vp, C.c_int, vp, vp]),
     "gp_compact_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_compact_active": (C.c_int, [vp, i64, i64, vp, vp, vp, sz, vp]),
+    "gp_compact_candidates": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, sz, vp]),
     "gp_sample_ranks_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
     "gp_sample_ranks": (C.c_int, [C.POINTER(u64), i64, vp, vp, sz, vp]),
     "gp_assign_workspace_bytes": (C.c_int, [i64, C.POINTER(sz)]),
@@ -160,7 +161,7 @@ def check(rc: int, what: str = "") -> None:
 # counted as one histogram pass plus one launch per 8-bit digit pass
 KERNELS_PER_CALL = {
     "gp_box_minmax": 2, "gp_weight_probe": 1, "gp_hilbert_keys": 1, "gp_sort_pairs": 9,
-    "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 1,
+    "gp_gather_points": 1, "gp_gather_rows": 1, "gp_compact_active": 1, "gp_compact_candidates": 1,
     "gp_assign_round": 2, "gp_rebase_bounds": 1, "gp_audit": 1, "gp_movement_fold": 13,
     "gp_scatter_by_gid": 1, "gp_deliver_permutation": 4, "gp_gather_ranks": 1,
     "gp_group_boxes": 1,

@@ -368,7 +368,8 @@ constexpr int CPER = 16;            // consecutive entries per thread (32: 44 vs
 constexpr int CT = CTH * CPER;      // entries per tile
 constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = ST_AGG - 1;
 
-__global__ void __launch_bounds__(CTH) compact_onepass(const int32_t* __restrict__ rank, int64_t n,
+__global__ void __launch_bounds__(CTH) compact_onepass(const int32_t* __restrict__ rank,
+                                                       const int32_t* __restrict__ pos, int64_t n,
                                                        int64_t size, int64_t ntiles,
                                                        unsigned long long* __restrict__ ticket,
                                                        unsigned long long* __restrict__ status,
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(CTH) compact_onepass(const int32_t* __restrict
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
-      s_out[o++] = (int32_t)(e0 + j);
+      s_out[o++] = pos ? pos[e0 + j] : (int32_t)(e0 + j);
     }
     __syncthreads();
     const long long base = s_base;
@@ -710,6 +711,13 @@ int gp_compact_workspace_bytes(int64_t n, size_t* bytes) {
 
 int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx, int64_t* count,
                       void* workspace, size_t workspace_bytes, void* stream) {
+  return gp_compact_candidates(rank, nullptr, n, size, idx, count, workspace, workspace_bytes,
+                               stream);
+}
+
+int gp_compact_candidates(const int32_t* rank, const int32_t* positions, int64_t n, int64_t size,
+                          int32_t* idx, int64_t* count, void* workspace, size_t workspace_bytes,
+                          void* stream) {
   size_t need = 0;
   gp_compact_workspace_bytes(n, &need);
   GP_REQUIRE(workspace_bytes >= need, "gp_compact_active: workspace too small");
@@ -727,8 +735,8 @@ int gp_compact_active(const int32_t* rank, int64_t n, int64_t size, int32_t* idx
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t cap = (int64_t)sms * 6;
-  compact_onepass<<<(unsigned)(nt < cap ? nt : cap), CTH, 0, s>>>(rank, n, size, nt, ticket, status,
-                                                                 idx, count);
+  compact_onepass<<<(unsigned)(nt < cap ? nt : cap), CTH, 0, s>>>(rank, positions, n, size, nt,
+                                                                 ticket, status, idx, count);
   return check_launch("compact_active");
 }
 

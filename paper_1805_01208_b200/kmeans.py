@@ -712,12 +712,40 @@ class DevicePartitioner:
             a.scan_regions = full_scan_regions(self.n_global, self.settings.k)
             return self.n
         a.scan_regions = 1       # sparse warm-up sample: 256-entry units
-        N.call("gp_compact_active", self.rank_sfc.data_ptr(), self.n, size,
+        ranks, pos, cnt = self._sample_candidates(size)
+        N.call("gp_compact_candidates", ranks.data_ptr(), _ptr(pos), cnt, size,
                self.active_idx.data_ptr(), self.active_cnt.data_ptr(),
                self.compact_ws.data_ptr(), self.compact_ws.numel(), self.sh)
         m = int(self.active_cnt.item())
         a.list, a.m = self.active_idx.data_ptr(), m
         return m
+
+    # sample sizes below these limits are compacted from a candidate list (the positions
+    # and ranks of the entries with rank < limit, built once) instead of all n ranks
+    CANDIDATE_TIERS = (1 << 26, 1 << 22)
+
+    def _sample_candidates(self, size):
+        """(ranks, positions or None, count) to compact the sample `rank < size` from."""
+        if getattr(self, "cand_tiers", None) is None:
+            self.cand_tiers = []
+            ranks, pos, cnt = self.rank_sfc, None, self.n
+            for limit in self.CANDIDATE_TIERS:       # large to small, each from the last
+                if cnt < 8 * limit:
+                    continue
+                idx = torch.empty(limit, dtype=torch.int32, device=self.device)
+                N.call("gp_compact_candidates", ranks.data_ptr(), _ptr(pos), cnt, limit,
+                       idx.data_ptr(), self.active_cnt.data_ptr(), self.compact_ws.data_ptr(),
+                       self.compact_ws.numel(), self.sh)
+                c = int(self.active_cnt.item())
+                pos = idx[:c]
+                ranks = self.rank_sfc[pos.long()].contiguous()
+                cnt = c
+                self.cand_tiers.append((limit, ranks, pos, c))
+        best = (self.rank_sfc, None, self.n)
+        for limit, ranks, pos, c in self.cand_tiers:
+            if size <= limit:
+                best = (ranks, pos, c)
+        return best
 
     def _assign(self):
         if self.hier is not None and not self.lists_fresh and not self.walk:
@@ -1061,7 +1089,7 @@ class DevicePartitioner:
         """Drop every n-sized device buffer (the caller keeps only the result)."""
         for name in ("X", "W", "A", "UBLB", "A_d", "UBLB_d", "X_d", "W_d", "gids", "rank_sfc", "active_idx",
                      "assign_ws", "fold_ws", "compact_ws", "keys_sorted", "hier", "grid_start",
-                     "grid_items", "ubox", "rstate", "rpar"):
+                     "grid_items", "ubox", "rstate", "rpar", "cand_tiers"):
             if hasattr(self, name):
                 setattr(self, name, None)
 
