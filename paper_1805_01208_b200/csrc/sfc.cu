@@ -66,6 +66,38 @@ __global__ void box_kernel(const double* __restrict__ pts, int64_t n, int d, int
   }
 }
 
+// the common layout, AoS (n, 2) rows: 16-byte loads, four independent points per step
+__global__ void box_kernel_aos2(const double2* __restrict__ pts, int64_t n,
+                                unsigned long long* keys, int32_t* nonfinite) {
+  double lo0 = INFINITY, lo1 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY;
+  int bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      v[u] = (u == 0 || i < n) ? pts[i] : v[0];   // past the end: repeat the step's first point
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bad |= !isfinite(v[u].x) | !isfinite(v[u].y);
+      lo0 = fmin(lo0, v[u].x); hi0 = fmax(hi0, v[u].x);
+      lo1 = fmin(lo1, v[u].y); hi1 = fmax(hi1, v[u].y);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo0 = fmin(lo0, __shfl_xor_sync(FULL, lo0, o)); hi0 = fmax(hi0, __shfl_xor_sync(FULL, hi0, o));
+    lo1 = fmin(lo1, __shfl_xor_sync(FULL, lo1, o)); hi1 = fmax(hi1, __shfl_xor_sync(FULL, hi1, o));
+  }
+  bad = __any_sync(FULL, bad);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&keys[0], dkey(lo0)); atomicMin(&keys[1], dkey(lo1));
+    atomicMax(&keys[2], dkey(hi0)); atomicMax(&keys[3], dkey(hi1));
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
 __global__ void box_finalize(unsigned long long* keys, int d) {
   int j = threadIdx.x;
   if (j < 2 * d) {
@@ -571,7 +603,16 @@ int gp_box_minmax(const double* pts, int64_t n, int d, int64_t stride_pt, int64_
   GP_CUDA(cudaMemsetAsync(keys, 0xff, d * sizeof(double), s));
   GP_CUDA(cudaMemsetAsync(keys + d, 0x00, d * sizeof(double), s));
   GP_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s));
-  box_kernel<<<stride_grid(n), 256, 0, s>>>(pts, n, d, stride_pt, stride_dim, keys, nonfinite);
+  if (d == 2 && stride_pt == 2 && stride_dim == 1 && ((uintptr_t)pts & 15) == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (n + 1023) / 1024;
+    box_kernel_aos2<<<(unsigned)(want < sms * 8 ? want : sms * 8), 256, 0, s>>>(
+        (const double2*)pts, n, keys, nonfinite);
+  } else {
+    box_kernel<<<stride_grid(n), 256, 0, s>>>(pts, n, d, stride_pt, stride_dim, keys, nonfinite);
+  }
   box_finalize<<<1, 32, 0, s>>>(keys, d);
   return check_launch("box");
 }
