@@ -60,12 +60,19 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const K* __restrict__ ke
   for (int i = threadIdx.x; i < npass * kRadix; i += kThreads) sh[i] = 0;
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
-    const K k = keys[i];
-    for (int p = 0; p < npass; ++p) {
-      const int sft = shift0 + 8 * p;
-      const int nb = end_bit - sft < 8 ? end_bit - sft : 8;
-      atomicAdd(&sh[p * kRadix + digit_of(k, sft, (1u << nb) - 1)], 1u);
+  constexpr int HU = 4;   // keys in flight per thread
+  for (int64_t i0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; i0 < n; i0 += HU * stride) {
+    K k[HU];
+#pragma unroll
+    for (int u = 0; u < HU; ++u) k[u] = i0 + u * stride < n ? keys[i0 + u * stride] : (K)0;
+#pragma unroll
+    for (int u = 0; u < HU; ++u) {
+      if (i0 + u * stride >= n) break;
+      for (int p = 0; p < npass; ++p) {
+        const int sft = shift0 + 8 * p;
+        const int nb = end_bit - sft < 8 ? end_bit - sft : 8;
+        atomicAdd(&sh[p * kRadix + digit_of(k[u], sft, (1u << nb) - 1)], 1u);
+      }
     }
   }
   __syncthreads();
@@ -328,7 +335,7 @@ int grid_hist() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    g = sms * 4;
+    g = sms * 8;
   }
   return g;
 }

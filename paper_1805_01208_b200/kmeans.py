@@ -186,12 +186,11 @@ def sort_pairs(keys: torch.Tensor, vals: torch.Tensor | None, keys_out: torch.Te
     vals None means val = input index."""
     n = keys.shape[0]
     dev = keys.device
-    if vals is None:
-        vals = torch.arange(n, dtype=torch.int32, device=dev)
     ko = keys_out if keys_out is not None else torch.empty_like(keys)
     wsb = N.size_query("gp_sort_workspace_bytes", n)
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
-    N.call("gp_sort_pairs", keys.data_ptr(), vals.data_ptr(), ko.data_ptr(), vals_out.data_ptr(),
+    # vals None: the sort numbers the pairs itself (no n-sized index array to fill and read)
+    N.call("gp_sort_pairs", keys.data_ptr(), _ptr(vals), ko.data_ptr(), vals_out.data_ptr(),
            n, key_bits, ws.data_ptr(), wsb, stream)
 
 
@@ -454,13 +453,18 @@ class DevicePartitioner:
         return self
 
     # ------------------------------------------------------------ helpers
+    def _cold_bounds(self):
+        """ub~ = +inf, lb~ = 0 for every entry: one fill of the packed fp16 pair
+        (0x7C00 | 0 << 16) instead of two strided ones."""
+        self.UBLB.view(torch.int32).fill_(0x7C00)
+
     def _alloc_state(self):
         n, k, d, dev = self.n, self.settings.k, self.d, self.device
         self.A = torch.full((n,), -1, dtype=torch.int32, device=dev)
         # (ub~, lb~) fp16 pairs (scaled by bound_scale): ub~ = +inf (unassigned), lb~ = 0
         # (kmeans.py:146-147)
-        self.UBLB = torch.zeros((n, 2), dtype=torch.float16, device=dev)
-        self.UBLB[:, 0] = math.inf
+        self.UBLB = torch.empty((n, 2), dtype=torch.float16, device=dev)
+        self._cold_bounds()
         # influences (ping-pong) | inv2_lo | inv2_hi | moves   (float64)
         self.kstate = torch.empty(5 * k, dtype=torch.float64, device=dev)
         # device bound maps S[k] | T[k] | A | B | steps, and their float32 parameters
@@ -1055,8 +1059,7 @@ class DevicePartitioner:
         self.centers_d.copy_(torch.from_numpy(np.ascontiguousarray(state.centers)))
         self._build_grid(state.centers)
         self._set_influence(state.influence, reset=True)
-        self.UBLB[:, 0] = math.inf
-        self.UBLB[:, 1] = 0.0
+        self._cold_bounds()
         self.lists_fresh = False
         self._assign()
         return self.A
@@ -1281,8 +1284,7 @@ class DistributedPartitioner(DevicePartitioner):
         self.centers_d.copy_(torch.from_numpy(np.ascontiguousarray(state.centers)))
         self._build_grid(state.centers)
         self._set_influence(state.influence, reset=True)
-        self.UBLB[:, 0] = math.inf
-        self.UBLB[:, 1] = 0.0
+        self._cold_bounds()
         self.lists_fresh = False
         self._assign()
         return self.A

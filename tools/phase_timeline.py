@@ -33,6 +33,6 @@ prev_end = t0
 for a, b, name in ev:
     gap = a - prev_end
     if w0 <= a - t0 <= w1 and (b - a >= min_us or gap >= min_us / 4):
-        short = name.split("(")[0].replace("void ", "").replace("gp::", "")[-50:]
+        short = (name.split("(")[0].replace("void ", "").replace("gp::", "") or name)[-50:]
         print(f"{(a - t0) / 1e3:9.3f} ms  dur {(b - a) / 1e3:8.3f}  gap {gap / 1e3:7.3f}  {short}")
     prev_end = max(prev_end, b)
