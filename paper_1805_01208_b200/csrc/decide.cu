@@ -2,6 +2,8 @@
 // (kmeans.py:425-443) on the device, so the host loop reads back a six-double
 // record per round instead of doing the k-sized control math itself
 // (d = 2 with exact block weights).
+#include <cmath>
+
 #include "common.cuh"
 
 namespace gp {
@@ -15,9 +17,13 @@ __global__ void __launch_bounds__(1024) balance_decide_kernel(
   __shared__ double s_tgt, s_cap;
   __shared__ int s_stop;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // wscale is a power of two (the exact weight scale 2^s), so multiplying by its inverse
+  // gives the bits of blk_int.astype(float64) / scale
+  const double winv = 1.0 / wscale;
   double sum = 0.0, mx = -INFINITY;
+#pragma unroll 8
   for (int c = tid; c < k; c += blockDim.x) {
-    const double w = (double)red[c] / wscale;   // blk_int.astype(float64) / scale
+    const double w = (double)red[c] * winv;
     sum += w;
     mx = fmax(mx, w);
   }
@@ -79,8 +85,9 @@ __global__ void __launch_bounds__(1024) balance_decide_kernel(
   __syncthreads();
   if (!s_stop) {
     const double lo = 1.0 - s_cap, hi = 1.0 + s_cap, tgt = s_tgt;
+#pragma unroll 4
     for (int c = tid; c < k; c += blockDim.x) {
-      const double w = (double)red[c] / wscale;
+      const double w = (double)red[c] * winv;
       const double gamma = w > 0.0 ? tgt / w : INFINITY;
       const double f = fmin(fmax(__dsqrt_rn(gamma), lo), hi);   // clip(gamma ** 0.5)
       next[c] = cur[c] * f;
@@ -95,6 +102,10 @@ extern "C" int gp_balance_decide(const long long* red, int k, double wscale, dou
                                  double* infl_next, void* stream) {
   GP_REQUIRE(red && bal && infl_cur && infl_next && k >= 1 && max_rounds >= 1 && wscale > 0,
              "gp_balance_decide: bad args");
+  {
+    int e = 0;
+    GP_REQUIRE(frexp(wscale, &e) == 0.5, "gp_balance_decide: wscale must be a power of two");
+  }
   gp::balance_decide_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
       red, k, wscale, eps, max_rounds, bal, infl_cur, infl_next);
   return gp::check_launch("balance_decide");
