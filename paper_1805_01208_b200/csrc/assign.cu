@@ -1250,13 +1250,13 @@ __global__ void group_boxes_kernel(const double* __restrict__ X, int64_t ldx,
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) group_candidates_kernel(
+__global__ void __launch_bounds__(1024) group_candidates_kernel(
     const double* __restrict__ boxes, int k, const double* __restrict__ centers,
     const double* __restrict__ inv2_lo, const double* __restrict__ inv2_hi,
     const int32_t* __restrict__ parent_list, const int32_t* __restrict__ parent_count,
     int parent_cap, int ratio_log2, int32_t* __restrict__ list, int32_t* __restrict__ count,
     int cap) {
-  __shared__ double s_two[2][8];
+  __shared__ double s_two[2][32];
   __shared__ int s_n;
   const int64_t g = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1837,12 +1837,18 @@ int gp_group_candidates(const double* boxes, int64_t ngroups, int d, int k,
           parent_ratio_log2, list, count, cap);
     return check_launch("group_candidates");
   }
+  // a few groups walking long sources (the top level over all k centers, warm-up samples):
+  // 1024 threads per group, so that the walk is four times shorter
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int threads = ngroups <= 2 * sms ? 1024 : 256;
   if (d == 2)
-    group_candidates_kernel<2><<<(unsigned)ngroups, 256, 0, s>>>(
+    group_candidates_kernel<2><<<(unsigned)ngroups, threads, 0, s>>>(
         boxes, k, centers, inv2_lo, inv2_hi, parent_list, parent_count, parent_cap,
         parent_ratio_log2, list, count, cap);
   else
-    group_candidates_kernel<3><<<(unsigned)ngroups, 256, 0, s>>>(
+    group_candidates_kernel<3><<<(unsigned)ngroups, threads, 0, s>>>(
         boxes, k, centers, inv2_lo, inv2_hi, parent_list, parent_count, parent_cap,
         parent_ratio_log2, list, count, cap);
   return check_launch("group_candidates");
