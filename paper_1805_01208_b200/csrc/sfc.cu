@@ -348,8 +348,27 @@ __global__ void gather_points_kernel(const double* __restrict__ pts, int64_t sp,
                                      const uint32_t* __restrict__ gids, int64_t n,
                                      double* __restrict__ X, int64_t ldx,
                                      const double* __restrict__ w_in, int wmode, void* w_out) {
-  constexpr int U = 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (d == 2 && ldx == 2 && sp == 2 && sd == 1 && wmode == GP_W_UNIT &&
+      (((uintptr_t)pts | (uintptr_t)X) & 15) == 0) {
+    // the common layout: one 16-byte load and store per point, eight gathers in flight
+    constexpr int UA = 8;
+    const double2* src = reinterpret_cast<const double2*>(pts);
+    double2* dst = reinterpret_cast<double2*>(X);
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += UA * stride) {
+      uint32_t g[UA];
+#pragma unroll
+      for (int u = 0; u < UA; ++u) g[u] = i0 + u * stride < n ? gids[i0 + u * stride] : 0u;
+      double2 v[UA];
+#pragma unroll
+      for (int u = 0; u < UA; ++u) v[u] = src[g[u]];
+#pragma unroll
+      for (int u = 0; u < UA; ++u)
+        if (i0 + u * stride < n) dst[i0 + u * stride] = v[u];
+    }
+    return;
+  }
+  constexpr int U = 4;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
     int64_t g[U];
 #pragma unroll
