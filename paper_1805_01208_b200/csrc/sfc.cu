@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(512) deliver_window_kernel(const uint32_t* __r
 
 __global__ void gather_ranks_kernel(const int32_t* __restrict__ r, const uint32_t* __restrict__ g,
                                     int64_t n, int32_t* __restrict__ out) {
-  constexpr int U = 4;
+  constexpr int U = 8;   // random 4-byte gathers in flight per thread
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
     uint32_t gg[U];
