@@ -5,7 +5,6 @@ import math
 import os
 import sys
 
-import numpy as np
 import pytest
 
 import graphio_cases as G

@@ -3,7 +3,6 @@
 the tokenizer's decimal -> binary64 conversion (host build of the kernel's code) against
 Python's float()."""
 import ctypes
-import io
 import random
 import struct
 
